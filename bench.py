@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Benchmark of the CG hot path of arXiv 1505.07630 on B200 (BASELINE.json metric:
+"CG iter/s & effective HBM GB/s, 256^3 Poisson LDU, at 1/2/4/8 B200").
+
+One step = one ``pcg_solve`` (or ``pipecg_solve``) of ``--iters`` fixed iterations (tol = 0) on
+the resident config-3 system: laplacianFoam 3-D 256^3 Poisson, FV Dirichlet walls, hot-face
+RHS, x0 = 0.  With N ranks the same global system is split into N contiguous z-slabs (halo
+exchange + reductions over NVLink), so the work is fixed as N grows ("strong").  value = global
+CG iterations per second (max over ranks of the device time).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--solver pcg|pipecg] [--impl reference]
+
+Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CG iter/s & effective HBM GB/s, 256³ Poisson LDU, at 1/2/4/8 B200"
+UNIT = "iter/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--solver", default="pcg", choices=["pcg", "pipecg"])
+    p.add_argument("--n", type=int, default=256, help="mesh is n^3 (config 3: 256)")
+    p.add_argument("--iters", type=int, default=200, help="fixed CG iterations per step")
+    p.add_argument("--batch", type=int, default=0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-profile", action="store_true", help="skip per-pass event timing")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------------------------------
+# byte model
+# ------------------------------------------------------------------------------------------
+def model_bytes(solver, N, F, P):
+    """Algorithmic bytes per iteration, LDU model: fp64 values, int32 addressing."""
+    if solver == "pcg":
+        return 88 * N + 16 * F + 28 * P
+    return 136 * N + 16 * F + 28 * P
+
+
+def pass_model_bytes(solver, N, F):
+    """Dominant kernel per launch, §8(d): classical pass A = 56N + 16F; pipelined pass U = 112N."""
+    return 56 * N + 16 * F if solver == "pcg" else 112 * N
+
+
+def pass_format_bytes(solver, info, N):
+    """Bytes the dominant kernel must move in the layout it actually streams."""
+    if solver == "pipecg":
+        return 112 * N
+    if info["layout_name"] == "DIA_SYM":
+        return 56 * N + 8 * info["nDiagonals"] * N  # r, rD, p_old, x in; p, q, x out; U_k once
+    return 56 * N + 12 * info["storedEntries"] + 12 * ((N + 31) // 32)
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(solver, n, world):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
+    committed `ncu --set full` capture summary (profiles/ncu_traffic.json), if it matches."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        e = d.get(f"{solver}_n{n}_p{world}")
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle baseline (tests/bench only may call oracle/)
+# ------------------------------------------------------------------------------------------
+def oracle_iter_rate(sys_, b, solver, k1, k2):
+    """Oracle per-iteration time from fixed-iteration runs (t(k2) - t(k1)) / (k2 - k1)."""
+    import oracle
+    fn = oracle.pcg if solver == "pcg" else oracle.pipecg
+    ts = []
+    for k in (k1, k2):
+        t0 = time.perf_counter()
+        fn(sys_, b, tol=0.0, maxIter=k)
+        ts.append(time.perf_counter() - t0)
+    per = (ts[1] - ts[0]) / (k2 - k1)
+    return 1.0 / per, per
+
+
+def build_global(n):
+    import meshgen
+    sys_ = meshgen.hex_laplacian(n, n, n, dirichlet=dict(x0=1.0))
+    return sys_, sys_.b
+
+
+def config_dict(args, world, info=None):
+    d = {"workload": f"c3: laplacianFoam 3-D {args.n}^3 Poisson ({args.n ** 3:,} cells), FV "
+                     f"Dirichlet walls, hot-face RHS, x0 = 0, {'Jacobi-PCG' if args.solver == 'pcg' else 'pipelined CG (Ghysels-Vanroose, Jacobi)'}, "
+                     f"{args.iters} fixed iterations per step (tol = 0)",
+         "cells": args.n ** 3, "solver": args.solver, "iters_per_step": args.iters,
+         "decomposition": f"{world} contiguous z-slab(s)",
+         "l2": "inputs larger than L2 (working set >= 1.9 GB vs 126 MB L2); no flush needed"}
+    if info is not None:
+        d["layout"] = info["layout_name"]
+    return d
+
+
+# ------------------------------------------------------------------------------------------
+# reference arm: the CPU oracle as it stands
+# ------------------------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    sys_, b = build_global(args.n)
+    fn = oracle.pcg if args.solver == "pcg" else oracle.pipecg
+    k = 2  # bounded sample per step: 2 oracle iterations of the same 256^3 workload
+    for _ in range(args.warmup):
+        fn(sys_, b, tol=0.0, maxIter=k)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fn(sys_, b, tol=0.0, maxIter=k)
+    dt = time.perf_counter() - t0
+    value = args.steps * k / dt
+    sample = (f"each step = oracle {args.solver} (C, fp64, 1 thread) for {k} iterations on the "
+              f"full {args.n}^3 system incl. r0 setup")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": config_dict(args, 1),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+
+    import meshgen
+    import paper_1505_07630_b200 as ldu
+
+    torch.cuda.set_device(local)
+    dist = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [ldu.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = ldu.Comm(rank, world, uid[0], local)
+
+    n = args.n
+    if world == 1:
+        sys_ = meshgen.hex_laplacian(n, n, n, dirichlet=dict(x0=1.0))
+    else:
+        sys_ = meshgen.hex_laplacian_slab(n, n, n, world, rank, dirichlet=dict(x0=1.0))
+    N, F = sys_.nCells, sys_.nFaces
+    P = sum(len(i.faceCells) for i in sys_.interfaces)
+    A = ldu.LduMatrix.from_system(sys_, comm)
+    info = A.info()
+    stream = torch.cuda.current_stream()
+    A.set_stream(stream.cuda_stream)
+    b = torch.from_numpy(sys_.b).cuda()
+    x = torch.zeros_like(b)
+    solve = A.pcg_solve if args.solver == "pcg" else A.pipecg_solve
+    kw = dict(tol=0.0, maxIter=args.iters, batch=args.batch)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        x.zero_()
+        solve(b, x, **kw)
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    kernels = 0
+    pass_ms, pass_n = 0.0, 0
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        x.zero_()
+        st, it, res = solve(b, x, profile=not args.no_profile, **kw)
+        s = A.stats()
+        kernels += s["kernels"]
+        pass_ms += s["passMs"][0 if args.solver == "pcg" else 1]
+        pass_n += s["passLaunches"][0 if args.solver == "pcg" else 1]
+    e1.record(stream)
+    barrier()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    clk = clocks.stop()
+    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    value = args.steps * args.iters / elapsed
+
+    # global byte model
+    tot = torch.tensor([N, F, P], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(tot)
+    Ng, Fg, Pg = (float(v) for v in tot.tolist())
+    bytes_iter = model_bytes(args.solver, Ng, Fg, Pg)
+    peak, peak_src = hbm_peak()
+
+    # roofline of the dominant kernel (this rank), measured live with CUDA events in the graph
+    roof = None
+    if pass_n:
+        t_launch = pass_ms / pass_n / 1e3
+        mb = pass_model_bytes(args.solver, N, F)
+        fb = pass_format_bytes(args.solver, info, N)
+        traffic = ncu_traffic(args.solver, n, world)
+        roof = {"kernel": "k_cg_passA" if args.solver == "pcg" else "k_pipe_U",
+                "bound": "hbm", "achieved": mb / t_launch / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": mb / t_launch / 1e9 / peak, "traffic": traffic,
+                "model_bytes_per_launch": mb, "launch_us": t_launch * 1e6,
+                "format_bytes_per_launch": fb, "format_achieved": fb / t_launch / 1e9,
+                "format_frac": fb / t_launch / 1e9 / peak, "peak_source": peak_src,
+                "share_of_step": pass_ms / 1e3 / elapsed}
+
+    # end to end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        bh = torch.from_numpy(sys_.b).pin_memory()
+        xh = torch.zeros(N, dtype=torch.float64).pin_memory()
+        for _ in range(2):
+            xh.zero_()
+            solve(bh, xh, **kw)
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        h2d = d2h = 0
+        for _ in range(args.steps):
+            xh.zero_()
+            solve(bh, xh, **kw)
+            s = A.stats()
+            h2d += s["h2dBytes"]
+            d2h += s["d2hBytes"]
+        f1.record(stream)
+        barrier()
+        te = torch.tensor([f0.elapsed_time(f1) / 1e3], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": args.steps * args.iters / float(te.item()), "unit": UNIT,
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        k1, k2 = 3, 15
+        rate, per = oracle_iter_rate(sys_, sys_.b, args.solver, k1, k2)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"oracle {args.solver} (C, fp64, -O2, 1 thread) on the same {n}^3 system: "
+                         f"(t({k2} it) - t({k1} it)) / {k2 - k1}",
+               "effective_gbps": rate * bytes_iter / 1e9}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": max(3, args.warmup),
+               "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": config_dict(args, world, info),
+               "effective_gbps": value * bytes_iter / 1e9,
+               "effective_frac_of_hbm": value * bytes_iter / 1e9 / peak,
+               "bytes_per_iter_model": bytes_iter,
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels,
+               "clocks": clk, "last_status": int(st), "iterations_per_step": it}
+        print(json.dumps(out), flush=True)
+    A.close()
+    if comm is not None:
+        comm.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

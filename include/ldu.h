@@ -1,0 +1,199 @@
+/*
+ * ldu.h -- C ABI of the B200-native hot path of arXiv 1505.07630 (AlOnazi, Keyes, Lastovetsky,
+ * Rychkov, "Design and Optimization of OpenFOAM-based CFD Applications for Hybrid and
+ * Heterogeneous HPC Platforms", ParCFD 2014): the conjugate-gradient pressure/Poisson solve.
+ *
+ * Library: paper_1505_07630_b200/libldu_b200.so (hand-written CUDA for sm_100a + NCCL).
+ * Citations: "P:n" = PAPER.md line n, "S:n" = SPEC.md line n (reference text read at survey
+ * time); readings "Zn" are listed in DESIGN.md.
+ *
+ * Conventions for every entry point:
+ *   - returns ldu_status and never throws; on error ldu_last_error() gives a message
+ *     (thread-local, valid until the next call on the same thread);
+ *   - a handle is bound to the CUDA device that was current at ldu_setup (or the comm's device)
+ *     and is NOT thread-safe: one handle per rank/device;
+ *   - all vectors are fp64 (double), all indices int32 (OpenFOAM "label");
+ *   - "host or device" pointer arguments are classified with cudaPointerGetAttributes; device
+ *     pointers must live on the handle's device (e.g. torch CUDA tensors); host pointers may be
+ *     pageable or pinned (pinned is faster);
+ *   - across ranks (comm != NULL) ldu_amul and the solves are COLLECTIVE: every rank calls them
+ *     in the same order with the same tol / maxIter / options.
+ */
+#ifndef LDU_B200_H
+#define LDU_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LDU_ABI_VERSION 1
+
+typedef enum {
+  LDU_OK = 0,                /* converged: finalRes < tol (or r == 0 exactly; reading Z2)         */
+  LDU_NOT_CONVERGED = 1,     /* maxIter reached; x = last iterate; *finalRes >= tol (non-fatal)   */
+  LDU_BREAKDOWN = 2,         /* (p,Ap) <= 0, delta - beta*gamma/alpha_old <= 0 or non-finite
+                                (reading Z19); x = last valid iterate, *nIter names the iteration */
+  LDU_ERR_INVALID_ARG = -1,  /* null pointer, nCells <= 0, nFaces < 0, index outside
+                                [0, nCells), lowerAddr == upperAddr, diag <= 0 or non-finite,
+                                maxIter < 0, tol < 0 or NaN, unknown option value            */
+  LDU_ERR_CUDA = -2,         /* a CUDA runtime error (message in ldu_last_error)                 */
+  LDU_ERR_NCCL = -3,         /* an NCCL error                                                    */
+  LDU_ERR_OOM = -4,          /* device allocation failed                                         */
+  LDU_ERR_STATE = -5         /* call not valid in the current state (e.g. history not recorded) */
+} ldu_status;
+
+typedef struct ldu_handle_s *ldu_handle; /* device layout, work vectors, graphs, streams       */
+typedef struct ldu_comm_s *ldu_comm;     /* two NCCL communicators + their streams; NULL = 1 rank */
+
+/* One processor interface ("halo-layer approach ... duplicates the cells next to a
+ * processor boundary"; OpenFOAM processor patch).  faceCells[i] is the local cell next to patch
+ * face i; coeffs[i] is OpenFOAM's interfaceBouCoeffs, i.e. the NEGATED off-diagonal, so the
+ * interface contribution to y = A x is  y[faceCells[i]] -= coeffs[i] * x_neighbour[i]  (reading
+ * Z10), where x_neighbour[i] is the neighbour rank's x at ITS faceCells[i] of the interface back
+ * to this rank (both sides list shared faces in the same order, reading Z22).  Several
+ * interfaces may name the same neighbour rank: they pair up in list order.  Host or device
+ * pointers; copied by ldu_setup. */
+typedef struct {
+  int neighbRank;
+  int nFaces;
+  const int *faceCells;   /* [nFaces] */
+  const double *coeffs;   /* [nFaces] */
+} ldu_interface;
+
+typedef struct {
+  int nInterfaces;
+  const ldu_interface *list; /* [nInterfaces] (host memory) */
+  ldu_comm comm;             /* required when nInterfaces > 0 or when nRanks > 1 */
+} ldu_interfaces;
+
+/* ---- multi-GPU plumbing (P:95 one process per device) ---------------------- */
+
+/* Writes a 128-byte NCCL unique id into id128 (call on rank 0, broadcast the bytes with
+ * torch.distributed).  Errors: LDU_ERR_INVALID_ARG (NULL), LDU_ERR_NCCL. */
+ldu_status ldu_get_unique_id(void *id128);
+
+/* Creates the rank's communicators (one for reductions, one for halo exchange) on cudaDevice.
+ * Collective over nRanks processes.  Errors: INVALID_ARG, CUDA, NCCL. */
+ldu_status ldu_comm_init(int rank, int nRanks, const void *id128, int cudaDevice, ldu_comm *out);
+ldu_status ldu_comm_destroy(ldu_comm comm);
+
+/* ---- setup ------------------------------------------------------------- */
+
+/* Builds the device layout of an OpenFOAM lduMatrix (P:206 names lduMatrix; semantics in
+ * SURVEY App. A): A[c][c] = diag[c], A[l[f]][u[f]] = upper[f], A[u[f]][l[f]] = lower[f]
+ * (lower == NULL => symmetric, lower := upper).  Local owned rows only ("the local matrix
+ * row dimension is number of cells within the subdomain"); couplings to other ranks come through
+ * `interfaces`.  Faces need not be sorted (reading Z10); duplicate faces are allowed (summed).
+ *
+ *   nCells   > 0, nFaces >= 0 (int32; 2*nFaces < 2^31)
+ *   lowerAddr, upperAddr [nFaces] int32 in [0, nCells), lowerAddr[f] != upperAddr[f]
+ *   diag [nCells] > 0 and finite (Jacobi preconditioner M = diag(A), reading Z9)
+ *   lower [nFaces] or NULL, upper [nFaces]
+ *   interfaces: NULL for a single-rank matrix.
+ * All arrays may be host or device pointers and are copied: the caller may free them on return.
+ * The one-time conversion runs on the device; it chooses a row-gathered, cell-ordered layout
+ * (DESIGN.md "Data layout"): symmetric banded matrices get a symmetric diagonal (DIA) layout
+ * storing each face coefficient once; others a SELL-32 layout.  Both are deterministic: SpMV
+ * sums diag first, then the row's entries in ascending column order, with no atomics.
+ * Errors: INVALID_ARG (message names the first offending index), CUDA, OOM. */
+ldu_status ldu_setup(int nCells, int nFaces, const int *lowerAddr, const int *upperAddr,
+                     const double *diag, const double *lower, const double *upper,
+                     const ldu_interfaces *interfaces, ldu_handle *out);
+
+/* Work stream for all subsequent calls on h (e.g. torch.cuda.current_stream().cuda_stream).
+ * NULL restores the handle's own stream.  The solves still return only after completion. */
+ldu_status ldu_set_stream(ldu_handle h, void *cudaStream);
+
+/* y = A x including processor interfaces ("point-to-point communication during the
+ * matrix-vector multiplication"; SURVEY §8(a) a2+a3).  x, y: [nCells] host or device, must not
+ * alias.  Collective when the handle has interfaces/comm.  Errors: INVALID_ARG, CUDA, NCCL. */
+ldu_status ldu_amul(ldu_handle h, const double *x, double *y);
+
+/* ---- solvers ----------------------------------------------------------------------------- */
+
+/* Jacobi-preconditioned classical CG (Eq 4): per iteration one
+ * SpMV with halo exchange and TWO global reductions ((p,q), then {(r,z),(r,r)} fused; reading
+ * Z4).  b: [nCells] host or device (not modified); x: [nCells] host or device, IN/OUT (initial
+ * guess in, solution out; reading Z8).  tol >= 0 applies to the criterion of the options (default
+ * ||r||_2/||b||_2, reading Z1); tol = 0 runs exactly maxIter iterations (fixed-iteration
+ * benchmarking).  Outputs: *nIter = number of x-updates (0 if the initial residual passes),
+ * *finalRes = criterion value of the last recurrence residual.  If ||b||_2 == 0: x = 0,
+ * nIter = 0, finalRes = 0.  Returns LDU_OK / LDU_NOT_CONVERGED / LDU_BREAKDOWN or an error. */
+ldu_status pcg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,
+                     int *nIter, double *finalRes);
+
+/* Ghysels-Vanroose pipelined CG with M = diag(A) ("only one collective communication per
+ * loop body ... overlapped by the sparse matrix-vector multiplication"; SURVEY
+ * §8(c) c3 Jacobi-specialised form): ONE fused reduction of (gamma, delta, ||r||^2) per
+ * iteration, overlapped with the SpMV and its halo exchange.  Same arguments and semantics as
+ * pcg_solve; the convergence test uses r_i at the top of iteration i (reading Z3). */
+ldu_status pipecg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,
+                        int *nIter, double *finalRes);
+
+#define LDU_NORM_L2 0        /* ||r||_2 / ||b||_2 (default, reading Z1)                          */
+#define LDU_NORM_OPENFOAM 1  /* sum|r| / (sum|A x0 - xbar sumA| + sum|b - xbar sumA| + 1e-20)    */
+
+typedef struct {
+  int norm;          /* LDU_NORM_L2 or LDU_NORM_OPENFOAM                                        */
+  int recordHistory; /* 1: keep the criterion value of every iteration (ldu_get_residual_history) */
+  int batch;         /* iterations per CUDA-graph launch; 0 = library default                   */
+  int profile;       /* 1: bracket each pass kernel with CUDA events inside the graph and report
+                        per-pass device time in ldu_solve_stats.passMs (one host sync per batch) */
+  int reserved[4];   /* must be zero                                                            */
+} ldu_solve_opts;
+
+ldu_status pcg_solve_ex(ldu_handle h, const double *b, double *x, double tol, int maxIter,
+                        const ldu_solve_opts *opts, int *nIter, double *finalRes);
+ldu_status pipecg_solve_ex(ldu_handle h, const double *b, double *x, double tol, int maxIter,
+                           const ldu_solve_opts *opts, int *nIter, double *finalRes);
+
+/* Residual history of the last solve with recordHistory = 1: hostOut[0..*n-1] = criterion at
+ * iterations 0..nIter (res0 first).  *n = min(cap, nIter + 1).  LDU_ERR_STATE if not recorded. */
+ldu_status ldu_get_residual_history(ldu_handle h, double *hostOut, int cap, int *n);
+
+typedef struct {
+  double solveMs;        /* device time of the last solve (CUDA events, whole call)            */
+  double iterMs;         /* device time of its iteration loop only (excludes r0 and finalize)  */
+  long long kernels;     /* kernel launches of this library in the last call (graph nodes incl.) */
+  long long allreduces;  /* global reductions issued in the last solve (per rank)              */
+  long long haloBytes;   /* halo bytes sent by this rank in the last call                      */
+  long long h2dBytes;    /* host->device bytes copied for b/x in the last call                 */
+  long long d2hBytes;    /* device->host bytes copied for x in the last call                   */
+  int iterations;        /* nIter of the last solve                                            */
+  int reserved;
+  double passMs[2];      /* profile = 1: summed device time of pass 0 (classical A / pipelined S)
+                            and pass 1 (classical B / pipelined U) over all iterations           */
+  long long passLaunches[2]; /* number of timed launches of each pass                          */
+} ldu_solve_stats;
+
+ldu_status ldu_get_solve_stats(ldu_handle h, ldu_solve_stats *out);
+
+#define LDU_LAYOUT_DIA_SYM 1  /* symmetric diagonal layout: offsets d_k, coefficient U_k[c] of
+                                 face (c, c + d_k); each face stored once                      */
+#define LDU_LAYOUT_SELL32 2   /* SELL-32: 32-row slices, per-slice width, lane-interleaved pairs */
+
+typedef struct {
+  int layout;            /* LDU_LAYOUT_*                                                        */
+  int nDiagonals;        /* DIA: number of offsets                                              */
+  int offsets[8];        /* DIA: ascending offsets                                              */
+  long long storedEntries; /* off-diagonal entries stored (incl. padding)                       */
+  long long matrixBytes;   /* device bytes of the matrix layout (incl. diag and 1/diag)         */
+  int nCells, nFaces, nInterfaceFaces, nRanks, rank;
+  int gridBlocks, blockThreads;
+} ldu_info;
+
+ldu_status ldu_get_info(ldu_handle h, ldu_info *out);
+
+/* fp64 STREAM triad a = b + s*c over n elements ("our implementation of the STREAM
+ * benchmark"), repeated `reps` times on the handle's device; *gbps = best 24*n bytes / time.
+ * Roofline denominator cross-check.  Uses its own scratch allocation. */
+ldu_status ldu_stream_triad(int device, long long n, int reps, double *gbps);
+
+ldu_status ldu_destroy(ldu_handle h);
+const char *ldu_last_error(void);
+int ldu_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LDU_B200_H */

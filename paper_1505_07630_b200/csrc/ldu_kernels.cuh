@@ -1,0 +1,254 @@
+// ldu_kernels.cuh -- device code of the CG hot path.
+//
+// Every streaming pass walks the rows in a grid-stride wavefront (block b handles rows
+// b*256 + t, then + gridDim*256, ...), so all blocks sweep the vectors together and the
+// neighbour gathers at +-nx*ny rows hit L2 instead of HBM; the grid is a multiple of the SM
+// count (occupancy-derived).  Reductions are deterministic: warp xor-butterfly, fixed-order block
+// tree, per-block partials in a fixed slot, and the last block to arrive sums the slots in index
+// order (no floating-point atomics anywhere).
+#pragma once
+
+#include "ldu_impl.cuh"
+
+namespace ldu {
+
+// ---------------------------------------------------------------------------------------------
+// row operators: s = init + sum_j a_cj * op(j) in ascending column order (diag term is `init`)
+// ---------------------------------------------------------------------------------------------
+template <int ND, class Op>
+__device__ __forceinline__ double row_apply(const DiaView<ND>& A, int c, double s, Op op) {
+#pragma unroll
+  for (int k = ND - 1; k >= 0; --k) {  // lower side: columns c - off[ND-1] < ... < c - off[0]
+    int j = c - A.off[k];
+    if (j >= 0) s = fma(__ldg(A.U[k] + j), op(j), s);
+  }
+#pragma unroll
+  for (int k = 0; k < ND; ++k) {  // upper side: columns c + off[0] < ... < c + off[ND-1]
+    int j = c + A.off[k];
+    if (j < A.n) s = fma(__ldg(A.U[k] + c), op(j), s);
+  }
+  return s;
+}
+
+template <class Op>
+__device__ __forceinline__ double row_apply(const SellView& A, int c, double s, Op op) {
+  const int slice = c >> 5, lane = c & 31;
+  const long long base = __ldg(A.slicePtr + slice);
+  const int np = __ldg(A.npairs + slice);
+  for (int jj = 0; jj < np; ++jj) {
+    const long long e = (base + jj) * 32 + lane;
+    const int2 cc = __ldg(A.col + e);
+    const double2 vv = __ldg(A.val + e);
+    if (cc.x < 0) break;
+    s = fma(vv.x, op(cc.x), s);
+    if (cc.y < 0) break;
+    s = fma(vv.y, op(cc.y), s);
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------------------------
+// deterministic reductions
+// ---------------------------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void warp_allreduce(double (&v)[NV]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+}
+
+// Sum over the block in a fixed tree; result in every lane of warp 0.
+template <int NV>
+__device__ __forceinline__ void block_reduce(double (&v)[NV], double (*sm)[32]) {
+  warp_allreduce<NV>(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sm[k][wid] = v[k];
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = lane < (int)(blockDim.x >> 5) ? sm[k][lane] : 0.0;
+    warp_allreduce<NV>(v);
+  }
+}
+
+// Block partial -> partials[k*ld + slot]; returns true in every thread of the last block to
+// arrive (of `nblocks` participating blocks).
+template <int NV>
+__device__ __forceinline__ bool store_partial_is_last(double (&v)[NV], double* partials, int ld,
+                                                      int slot, unsigned* ticket,
+                                                      unsigned nblocks) {
+  __shared__ double sm[NV][32];
+  __shared__ bool last;
+  block_reduce<NV>(v, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) partials[k * ld + slot] = v[k];
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    last = (t == nblocks - 1);
+  }
+  __syncthreads();
+  return last;
+}
+
+// In the last block: out[k] = sum of partials[k*ld + 0 .. total) in a fixed order.
+template <int NV>
+__device__ __forceinline__ void sum_partials(const double* partials, int ld, int total,
+                                             double* out, unsigned* ticket) {
+  __shared__ double sm[NV][32];
+  __threadfence();
+  double v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    v[k] = 0.0;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) v[k] += __ldcg(partials + k * ld + i);
+  }
+  block_reduce<NV>(v, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = v[k];
+    *ticket = 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// control steps (one thread; readings Z1-Z3, Z19)
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool converged(double res, double tol) { return res < tol || res == 0.0; }
+
+__device__ __forceinline__ double crit_value(const State* st, double v) {
+  return st->norm == LDU_NORM_L2 ? sqrt(v) / st->scale : v / st->scale;
+}
+
+__device__ __forceinline__ void record(State* st, int i, double res) {
+  st->res = res;
+  if (st->record && i < st->histCap) st->hist[i] = res;
+}
+
+__device__ __forceinline__ void finish(State* st, int status, int iter) {
+  st->done = 1;
+  st->status = status;
+  st->iter = iter;
+}
+
+// criterion scale from s0 = sum b^2 (L2) or the OpenFOAM normFactor sum
+__device__ __forceinline__ void ctl_scale(State* st, double s0) {
+  if (st->norm == LDU_NORM_L2) {
+    st->scale = sqrt(s0);
+    if (st->scale == 0.0) {  // b = 0 => x = 0 (reading Z1)
+      st->zero_x = 1;
+      record(st, 0, 0.0);
+      finish(st, LDU_OK, 0);
+    }
+  } else {
+    st->scale = s0 + 1e-20;
+  }
+}
+
+// classical, after r0: s = [scale piece, (r0, z0), crit piece(r0)]
+__device__ __forceinline__ void ctl_cg_init(State* st, const double* s) {
+  ctl_scale(st, s[0]);
+  if (st->done) return;
+  const double res = crit_value(st, s[2]);
+  record(st, 0, res);
+  st->iter = 0;
+  st->k = 0;
+  st->rho = s[1];
+  st->alpha = 0.0;
+  st->beta = 0.0;
+  st->xpending = 0;
+  if (converged(res, st->tol)) finish(st, LDU_OK, 0);
+  else if (st->maxIter == 0) finish(st, LDU_NOT_CONVERGED, 0);
+}
+
+// classical, after pass A_k: s = [(p_k, A p_k)]
+__device__ __forceinline__ void ctl_cg_A(State* st, const double* s) {
+  const double pq = s[0];
+  st->xpending = 0;  // pass A_k applied alpha_{k-1} p_{k-1}: x = x_k
+  if (!(pq > 0.0) || !isfinite(pq)) {
+    finish(st, LDU_BREAKDOWN, st->k);
+    return;
+  }
+  st->alpha = st->rho / pq;
+}
+
+// classical, after pass B_k: s = [(r_{k+1}, z_{k+1}), crit piece(r_{k+1})]
+__device__ __forceinline__ void ctl_cg_B(State* st, const double* s) {
+  const int it = st->k + 1;
+  st->iter = it;
+  st->xpending = 1;  // alpha_k p_k still to be added to x
+  const double res = crit_value(st, s[1]);
+  record(st, it, res);
+  if (converged(res, st->tol)) finish(st, LDU_OK, it);
+  else if (it >= st->maxIter) finish(st, LDU_NOT_CONVERGED, it);
+  else {
+    st->beta = s[0] / st->rho;
+    st->rho = s[0];
+    st->k = it;
+  }
+}
+
+// pipelined, top of iteration i = st->k: s = [gamma_i, delta_i, crit piece(r_i)]
+__device__ __forceinline__ void ctl_pipe_top(State* st, const double* s) {
+  const int i = st->k;
+  const double res = crit_value(st, s[2]);
+  record(st, i, res);
+  st->iter = i;
+  if (converged(res, st->tol)) { finish(st, LDU_OK, i); return; }
+  if (i >= st->maxIter) { finish(st, LDU_NOT_CONVERGED, i); return; }
+  const double g = s[0], d = s[1];
+  double a, b;
+  if (i == 0) {
+    b = 0.0;
+    if (!(d > 0.0) || !isfinite(d)) { finish(st, LDU_BREAKDOWN, i); return; }
+    a = g / d;
+  } else {
+    b = g / st->gamma_old;
+    const double den = d - b * g / st->alpha_old;
+    if (!(den > 0.0) || !isfinite(den)) { finish(st, LDU_BREAKDOWN, i); return; }
+    a = g / den;
+  }
+  st->pa = a;
+  st->pb = b;
+  st->gamma_old = g;
+  st->alpha_old = a;
+}
+
+// control selector for the "last block" epilogue of a pass (single rank) or the ctl kernel
+enum Ctl : int { CTL_NONE = 0, CTL_CG_INIT, CTL_PIPE_SCALE, CTL_XBAR, CTL_CG_A, CTL_CG_B,
+                 CTL_PIPE_TOP, CTL_PIPE_NEXT };
+
+__device__ __forceinline__ void run_ctl(int ctl, State* st, const double* s) {
+  switch (ctl) {
+    case CTL_CG_INIT: ctl_cg_init(st, s); break;
+    case CTL_PIPE_SCALE: ctl_scale(st, s[0]); break;
+    case CTL_XBAR: st->xbar = s[0] / s[1]; break;
+    case CTL_CG_A: ctl_cg_A(st, s); break;
+    case CTL_CG_B: ctl_cg_B(st, s); break;
+    case CTL_PIPE_TOP: ctl_pipe_top(st, s); break;
+    case CTL_PIPE_NEXT: st->k += 1; ctl_pipe_top(st, s); break;
+    default: break;
+  }
+}
+
+// Common epilogue: partials -> (last block) local sums -> (single rank) control step.
+struct RedArgs {
+  double* partials;
+  int ld;
+  unsigned* ticket;
+  double* sums;  // local sums (send buffer of the cross-rank allgather)
+  int ctl;       // control step to run here when single-rank, else CTL_NONE
+};
+
+template <int NV>
+__device__ __forceinline__ void epilogue(double (&v)[NV], const RedArgs& ra, State* st) {
+  if (store_partial_is_last<NV>(v, ra.partials, ra.ld, blockIdx.x, ra.ticket, gridDim.x)) {
+    sum_partials<NV>(ra.partials, ra.ld, gridDim.x, ra.sums, ra.ticket);
+    if (threadIdx.x == 0 && ra.ctl != CTL_NONE) run_ctl(ra.ctl, st, ra.sums);
+  }
+}
+
+}  // namespace ldu

@@ -1,0 +1,872 @@
+// ldu_solve.cu -- the hot path: SpMV, Jacobi-PCG and pipelined CG drivers.
+//
+// Classical Jacobi-PCG, two fused HBM passes per iteration:
+//   pass A_k : x += alpha_{k-1} p_{k-1};  p_k = rD.r + beta_k p_{k-1} (recomputed at every
+//              neighbour, never re-read);  q = A p_k;  partial (p_k, q)        -> control A (alpha)
+//   pass B_k : r -= alpha_k q;  partials (r, rD.r), crit(r)                    -> control B (beta, test)
+//   p is ping-pong buffered (pass A gathers p_{k-1} while writing p_k).
+// Pipelined CG (Ghysels-Vanroose, Jacobi form: u = rD.r, m = rD.w,
+// q = rD.s are never stored):
+//   pass S_i : n = A (rD.w)                      (overlaps the single allgather of the partials)
+//   control  : alpha_i, beta_i, convergence test on r_i
+//   pass U_i : z = n + b z; s = w + b s; p = rD.r + b p; x += a p; r -= a s; w -= a z;
+//              partials (r, rD.r), (w, rD.r), crit(r)  -> one fused reduction
+// Scalars never leave the device; iterations run as CUDA-graph batches whose kernels exit at
+// entry once the device `done` flag is set; the host reads the state once per batch.
+#include <cmath>
+#include <cstring>
+#include <cstdlib>
+#include <vector>
+
+#include "ldu_kernels.cuh"
+
+namespace ldu {
+
+namespace {
+
+// ---------------------------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------------------------
+#define GRID_STRIDE(c, n) \
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < (n); c += gridDim.x * blockDim.x)
+
+struct Red {  // reduction plumbing of one pass
+  double* partials;
+  int ld;
+  unsigned* ticket;
+  double* sums;
+  int ctl;         // control step run by the last block (single rank) or CTL_NONE
+  int slot_base;   // first partial slot of this kernel
+  int total;       // slots summed by the last block
+  int store_only;  // 1: store partials only (a later kernel finishes the reduction)
+};
+
+template <int NV>
+__device__ __forceinline__ void finish_reduction(double (&v)[NV], const Red& rd, State* st) {
+  if (rd.store_only) {
+    __shared__ double sm[NV][32];
+    block_reduce<NV>(v, sm);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) rd.partials[k * rd.ld + rd.slot_base + blockIdx.x] = v[k];
+    return;
+  }
+  if (store_partial_is_last<NV>(v, rd.partials, rd.ld, rd.slot_base + blockIdx.x, rd.ticket,
+                                gridDim.x)) {
+    sum_partials<NV>(rd.partials, rd.ld, rd.total, rd.sums, rd.ticket);
+    if (threadIdx.x == 0 && rd.ctl != CTL_NONE) run_ctl(rd.ctl, st, rd.sums);
+  }
+}
+
+// y = A x over internal faces (diag first, ascending columns).
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_amul(Fmt A, const double* __restrict__ diag,
+                                                 const double* __restrict__ x,
+                                                 double* __restrict__ y) {
+  GRID_STRIDE(c, A.n) {
+    y[c] = row_apply(A, c, __ldg(diag + c) * __ldg(x + c), [&](int j) { return __ldg(x + j); });
+  }
+}
+
+// Interface update (reading Z10, Z23): y[cell] -= sum_f coeff[f] * recv[f] for every
+// interface cell, contributions in interface order then face order.
+__global__ void k_iface_apply(int nIfCells, const int* __restrict__ cell,
+                              const int* __restrict__ ptr, const int* __restrict__ fidx,
+                              const double* __restrict__ coeff, const double* __restrict__ recv,
+                              double* __restrict__ y, const State* st) {
+  if (st && st->done) return;
+  GRID_STRIDE(i, nIfCells) {
+    double corr = 0.0;
+    for (int t = ptr[i]; t < ptr[i + 1]; ++t) corr = fma(coeff[fidx[t]], recv[fidx[t]], corr);
+    y[cell[i]] -= corr;
+  }
+}
+
+// Interface update of q = A p_k in pass A, plus the (p, q) correction partial.
+__global__ void __launch_bounds__(kBlock) k_iface_cg(int nIfCells, const int* __restrict__ cell,
+                                                     const int* __restrict__ ptr,
+                                                     const int* __restrict__ fidx,
+                                                     const double* __restrict__ coeff,
+                                                     const double* __restrict__ recv,
+                                                     double* __restrict__ q, const double* p0,
+                                                     const double* p1, State* st, Red rd) {
+  if (st->done) return;
+  const double* __restrict__ pnew = (st->k & 1) ? p1 : p0;
+  double v[1] = {0.0};
+  GRID_STRIDE(i, nIfCells) {
+    double corr = 0.0;
+    for (int t = ptr[i]; t < ptr[i + 1]; ++t) corr = fma(coeff[fidx[t]], recv[fidx[t]], corr);
+    const int c = cell[i];
+    q[c] -= corr;
+    v[0] -= pnew[c] * corr;
+  }
+  finish_reduction<1>(v, rd, st);
+}
+
+enum Pack : int { PACK_PLAIN = 0, PACK_SCALED = 1, PACK_CG_P = 2 };
+
+// Halo send buffer: the SpMV operand at the interface cells.
+__global__ void k_pack(int nIfFaces, const int* __restrict__ fc, int mode,
+                       const double* __restrict__ a, const double* __restrict__ rD,
+                       const double* p0, const double* p1, const State* st,
+                       double* __restrict__ send) {
+  if (st && st->done) return;
+  double beta = 0.0;
+  const double* pold = nullptr;
+  if (mode == PACK_CG_P) {
+    beta = st->beta;
+    pold = (st->k & 1) ? p0 : p1;
+  }
+  GRID_STRIDE(i, nIfFaces) {
+    const int c = fc[i];
+    double v = a[c];
+    if (mode == PACK_SCALED) v = rD[c] * v;
+    else if (mode == PACK_CG_P) v = fma(beta, pold[c], rD[c] * v);
+    send[i] = v;
+  }
+}
+
+__global__ void k_fill(int n, double v, double* __restrict__ y) {
+  GRID_STRIDE(c, n) y[c] = v;
+}
+
+// OpenFOAM norm, step 1: partials [sum x0, cell count] -> xbar (reading Z1)
+__global__ void __launch_bounds__(kBlock) k_sum_x(int n, const double* __restrict__ x, State* st,
+                                                  Red rd) {
+  double v[2] = {0.0, 0.0};
+  GRID_STRIDE(c, n) {
+    v[0] += x[c];
+    v[1] += 1.0;
+  }
+  finish_reduction<2>(v, rd, st);
+}
+
+// r = b - Ax (Ax precomputed incl. interfaces).  Partials:
+//   L2:       [sum b^2, (r, rD.r), sum r^2]
+//   OpenFOAM: [sum |Ax - xbar sumA| + |b - xbar sumA|, (r, rD.r), sum |r|]
+__global__ void __launch_bounds__(kBlock) k_resid(int n, const double* __restrict__ b,
+                                                  const double* __restrict__ Ax,
+                                                  const double* __restrict__ sumA,
+                                                  const double* __restrict__ rD,
+                                                  double* __restrict__ r, State* st, Red rd) {
+  const bool l2 = st->norm == LDU_NORM_L2;
+  const double xbar = st->xbar;
+  double v[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(c, n) {
+    const double bc = b[c], ax = Ax[c];
+    const double rc = bc - ax;
+    r[c] = rc;
+    if (l2) {
+      v[0] += bc * bc;
+      v[2] += rc * rc;
+    } else {
+      const double sa = xbar * sumA[c];
+      v[0] += fabs(ax - sa) + fabs(bc - sa);
+      v[2] += fabs(rc);
+    }
+    v[1] += rc * (rD[c] * rc);
+  }
+  finish_reduction<3>(v, rd, st);
+}
+
+// classical pass A_k (see file header)
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_cg_passA(Fmt A, const double* __restrict__ rD,
+                                                     const double* __restrict__ r, double* p0,
+                                                     double* p1, double* __restrict__ q,
+                                                     double* __restrict__ x, State* st, Red rd) {
+  if (st->done) return;
+  const int k = st->k;
+  const double beta = st->beta, alpha = st->alpha;
+  const double* __restrict__ pold = (k & 1) ? p0 : p1;
+  double* __restrict__ pnew = (k & 1) ? p1 : p0;
+  double v[1] = {0.0};
+  GRID_STRIDE(c, A.n) {
+    auto op = [&](int j) { return fma(beta, __ldg(pold + j), __ldg(rD + j) * __ldg(r + j)); };
+    const double po = __ldg(pold + c);
+    const double pc = fma(beta, po, __ldg(rD + c) * __ldg(r + c));
+    const double qc = row_apply(A, c, pc / __ldg(rD + c), op);
+    pnew[c] = pc;
+    q[c] = qc;
+    x[c] = fma(alpha, po, x[c]);
+    v[0] = fma(pc, qc, v[0]);
+  }
+  finish_reduction<1>(v, rd, st);
+}
+
+// classical pass B_k
+__global__ void __launch_bounds__(kBlock) k_cg_passB(int n, const double* __restrict__ rD,
+                                                     const double* __restrict__ q,
+                                                     double* __restrict__ r, State* st, Red rd) {
+  if (st->done) return;
+  const double alpha = st->alpha;
+  const bool l2 = st->norm == LDU_NORM_L2;
+  double v[2] = {0.0, 0.0};
+  GRID_STRIDE(c, n) {
+    const double rc = fma(-alpha, q[c], r[c]);
+    r[c] = rc;
+    v[0] = fma(rc, rD[c] * rc, v[0]);
+    v[1] += l2 ? rc * rc : fabs(rc);
+  }
+  finish_reduction<2>(v, rd, st);
+}
+
+// classical exit: x += alpha_k p_k if pending
+__global__ void k_cg_final(int n, const double* p0, const double* p1, double* __restrict__ x,
+                           const State* st) {
+  if (!st->xpending) return;
+  const double alpha = st->alpha;
+  const double* __restrict__ p = (st->k & 1) ? p1 : p0;
+  GRID_STRIDE(c, n) x[c] = fma(alpha, p[c], x[c]);
+}
+
+// out = A (rD.in) over internal faces; diag term diag*rD*in taken as in exactly.
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_spmv_scaled(Fmt A, const double* __restrict__ rD,
+                                                        const double* __restrict__ in,
+                                                        double* __restrict__ out,
+                                                        const State* st) {
+  if (st->done) return;
+  GRID_STRIDE(c, A.n) {
+    out[c] = row_apply(A, c, __ldg(in + c), [&](int j) { return __ldg(rD + j) * __ldg(in + j); });
+  }
+}
+
+// pipelined: partials [gamma = (r, rD.r), delta = (w, rD.r), crit(r)] over final r, w
+__global__ void __launch_bounds__(kBlock) k_pipe_dots(int n, const double* __restrict__ rD,
+                                                      const double* __restrict__ r,
+                                                      const double* __restrict__ w, State* st,
+                                                      Red rd) {
+  if (st->done) return;
+  const bool l2 = st->norm == LDU_NORM_L2;
+  double v[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(c, n) {
+    const double rc = r[c], u = rD[c] * rc;
+    v[0] = fma(rc, u, v[0]);
+    v[1] = fma(w[c], u, v[1]);
+    v[2] += l2 ? rc * rc : fabs(rc);
+  }
+  finish_reduction<3>(v, rd, st);
+}
+
+// pipelined pass U_i (see file header)
+__global__ void __launch_bounds__(kBlock) k_pipe_U(int n, const double* __restrict__ rD,
+                                                   const double* __restrict__ nv,
+                                                   double* __restrict__ z, double* __restrict__ s,
+                                                   double* __restrict__ p, double* __restrict__ x,
+                                                   double* __restrict__ r, double* __restrict__ w,
+                                                   State* st, Red rd) {
+  if (st->done) return;
+  const double a = st->pa, b = st->pb;
+  const bool l2 = st->norm == LDU_NORM_L2;
+  double v[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(c, n) {
+    const double rdc = rD[c], rc0 = r[c], wc0 = w[c];
+    const double zc = fma(b, z[c], nv[c]);
+    const double sc = fma(b, s[c], wc0);
+    const double pc = fma(b, p[c], rdc * rc0);
+    z[c] = zc;
+    s[c] = sc;
+    p[c] = pc;
+    x[c] = fma(a, pc, x[c]);
+    const double rc = fma(-a, sc, rc0);
+    const double wc = fma(-a, zc, wc0);
+    r[c] = rc;
+    w[c] = wc;
+    const double u = rdc * rc;
+    v[0] = fma(rc, u, v[0]);
+    v[1] = fma(wc, u, v[1]);
+    v[2] += l2 ? rc * rc : fabs(rc);
+  }
+  finish_reduction<3>(v, rd, st);
+}
+
+// multi-rank control: sum the allgathered per-rank sums in rank order, then run the step.
+__global__ void k_ctl(int ctl, State* st, const double* __restrict__ gsums, int nRanks, int nv) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (st->done && ctl != CTL_XBAR) return;
+  double s[kMaxVals] = {0.0, 0.0, 0.0, 0.0};
+  for (int r = 0; r < nRanks; ++r)
+    for (int k = 0; k < nv; ++k) s[k] += gsums[r * kMaxVals + k];
+  run_ctl(ctl, st, s);
+}
+
+__global__ void k_triad(long long n, double* __restrict__ a, const double* __restrict__ b,
+                        const double* __restrict__ c, double sc) {
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n / 2; i += stride) {
+    double2 bb = reinterpret_cast<const double2*>(b)[i];
+    double2 cc = reinterpret_cast<const double2*>(c)[i];
+    reinterpret_cast<double2*>(a)[i] = make_double2(fma(sc, cc.x, bb.x), fma(sc, cc.y, bb.y));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------------------------
+template <class F>
+void with_format(ldu_handle h, F&& f) {
+  if (h->layout == LDU_LAYOUT_SELL32) {
+    SellView v{h->n, h->slicePtr, h->npairs, h->col, h->val};
+    f(v);
+    return;
+  }
+  auto dia = [&](auto tag) {
+    constexpr int ND = decltype(tag)::value;
+    DiaView<ND> v;
+    v.n = h->n;
+    for (int k = 0; k < ND; ++k) {
+      v.off[k] = h->off[k];
+      v.U[k] = h->U + (size_t)k * h->n;
+    }
+    f(v);
+  };
+  switch (h->nd) {
+    case 1: dia(std::integral_constant<int, 1>()); break;
+    case 2: dia(std::integral_constant<int, 2>()); break;
+    case 3: dia(std::integral_constant<int, 3>()); break;
+    case 4: dia(std::integral_constant<int, 4>()); break;
+    case 5: dia(std::integral_constant<int, 5>()); break;
+    case 6: dia(std::integral_constant<int, 6>()); break;
+    case 7: dia(std::integral_constant<int, 7>()); break;
+    case 8: dia(std::integral_constant<int, 8>()); break;
+    default: throw Error(LDU_ERR_STATE, "bad DIA offset count");
+  }
+}
+
+int small_grid(long long n) {
+  long long b = (n + kBlock - 1) / kBlock;
+  return (int)std::max(1LL, std::min(b, 4096LL));
+}
+
+struct Launch {
+  ldu_handle h;
+  long long kernels = 0;
+  cudaStream_t s;
+};
+
+Red red_of(ldu_handle h, int ctl, bool single) {
+  Red r;
+  r.partials = h->partials;
+  r.ld = h->maxParts;
+  r.ticket = h->ticket;
+  r.sums = single ? h->gsums : h->sums;  // single rank: the local sums are the global sums
+  r.ctl = single ? ctl : CTL_NONE;
+  r.slot_base = 0;
+  r.total = h->grid;
+  r.store_only = 0;
+  return r;
+}
+
+bool multi(ldu_handle h) { return h->comm && h->comm->nRanks > 1; }
+
+// allgather of the local sums and the control step (multi-rank only)
+void allgather_ctl(ldu_handle h, int ctl, int nv, cudaStream_t s, long long& kernels) {
+  ldu_comm cm = h->comm;
+  CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+  CUDA_CHECK(cudaStreamWaitEvent(h->red_stream, h->ev_fork, 0));
+  NCCL_CHECK(ncclAllGather(h->sums, h->gsums, kMaxVals, ncclDouble, cm->red, h->red_stream));
+  CUDA_CHECK(cudaEventRecord(h->ev_red, h->red_stream));
+  CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_red, 0));
+  k_ctl<<<1, 32, 0, s>>>(ctl, h->st, h->gsums, cm->nRanks, nv);
+  ++kernels;
+  h->stats.allreduces++;
+}
+
+// halo exchange of the packed send buffer on the halo stream; returns after enqueueing.
+void halo_exchange(ldu_handle h, cudaStream_t s) {
+  CUDA_CHECK(cudaEventRecord(h->ev_pack, s));
+  CUDA_CHECK(cudaStreamWaitEvent(h->halo_stream, h->ev_pack, 0));
+  NCCL_CHECK(ncclGroupStart());
+  for (const DevInterface& it : h->ifaces) {
+    if (!it.nFaces) continue;
+    NCCL_CHECK(ncclSend(h->sendbuf + it.offset, it.nFaces, ncclDouble, it.neighbRank,
+                        h->comm->halo, h->halo_stream));
+    NCCL_CHECK(ncclRecv(h->recvbuf + it.offset, it.nFaces, ncclDouble, it.neighbRank,
+                        h->comm->halo, h->halo_stream));
+  }
+  NCCL_CHECK(ncclGroupEnd());
+  CUDA_CHECK(cudaEventRecord(h->ev_halo, h->halo_stream));
+  h->stats.haloBytes += 8LL * h->nIfFaces;
+}
+
+void wait_halo(ldu_handle h, cudaStream_t s) { CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_halo, 0)); }
+
+// y = A x including interfaces, all on stream s (x, y device, internal or user)
+void amul_dev(ldu_handle h, const double* x, double* y, cudaStream_t s, long long& kernels) {
+  const bool haveIf = h->nIfFaces > 0;
+  if (haveIf) {
+    k_pack<<<small_grid(h->nIfFaces), kBlock, 0, s>>>(h->nIfFaces, h->ifFaceCells, PACK_PLAIN, x,
+                                                      nullptr, nullptr, nullptr, nullptr, h->sendbuf);
+    ++kernels;
+    halo_exchange(h, s);
+  }
+  with_format(h, [&](auto A) { k_amul<<<h->grid, kBlock, 0, s>>>(A, h->diag, x, y); });
+  ++kernels;
+  if (haveIf) {
+    wait_halo(h, s);
+    k_iface_apply<<<small_grid(h->nIfCells), kBlock, 0, s>>>(
+        h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx, h->ifCoeffs, h->recvbuf, y, nullptr);
+    ++kernels;
+  }
+}
+
+void ensure_vec(double*& p, int n) {
+  if (!p) p = dmalloc<double>(n);
+}
+
+void ensure_work(ldu_handle h, bool pipelined) {
+  const int n = h->n;
+  ensure_vec(h->x, n);
+  ensure_vec(h->r, n);
+  ensure_vec(h->ybuf, n);
+  if (!pipelined) {
+    ensure_vec(h->p0, n);
+    ensure_vec(h->p1, n);
+    ensure_vec(h->q, n);
+  } else {
+    ensure_vec(h->w, n);
+    ensure_vec(h->nv, n);
+    ensure_vec(h->z, n);
+    ensure_vec(h->s, n);
+    ensure_vec(h->p0, n);
+  }
+}
+
+// One batch of `batch` iterations, enqueued on s (captured into a graph by the caller).
+void prof_mark(ldu_handle h, bool profile, int idx, cudaStream_t s) {
+  if (profile) CUDA_CHECK(cudaEventRecord(h->prof_ev[idx], s));
+}
+
+long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile) {
+  long long kernels = 0;
+  const bool mr = multi(h);
+  const bool haveIf = h->nIfFaces > 0;
+  for (int it = 0; it < batch; ++it) {
+    // pass A
+    if (haveIf) {
+      k_pack<<<small_grid(h->nIfFaces), kBlock, 0, s>>>(h->nIfFaces, h->ifFaceCells, PACK_CG_P,
+                                                        h->r, h->rD, h->p0, h->p1, h->st,
+                                                        h->sendbuf);
+      ++kernels;
+      halo_exchange(h, s);
+    }
+    Red ra = red_of(h, CTL_CG_A, !mr);
+    if (haveIf) ra.store_only = 1;
+    prof_mark(h, profile, 4 * it + 0, s);
+    with_format(h, [&](auto A) {
+      k_cg_passA<<<h->grid, kBlock, 0, s>>>(A, h->rD, h->r, h->p0, h->p1, h->q, h->x, h->st, ra);
+    });
+    prof_mark(h, profile, 4 * it + 1, s);
+    ++kernels;
+    if (haveIf) {
+      wait_halo(h, s);
+      Red ri = red_of(h, CTL_CG_A, !mr);
+      const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->grid);
+      ri.slot_base = h->grid;
+      ri.total = h->grid + ig;
+      k_iface_cg<<<ig, kBlock, 0, s>>>(h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx,
+                                       h->ifCoeffs, h->recvbuf, h->q, h->p0, h->p1, h->st, ri);
+      ++kernels;
+    }
+    if (mr) allgather_ctl(h, CTL_CG_A, 1, s, kernels);
+    // pass B
+    prof_mark(h, profile, 4 * it + 2, s);
+    k_cg_passB<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->q, h->r, h->st, red_of(h, CTL_CG_B, !mr));
+    prof_mark(h, profile, 4 * it + 3, s);
+    ++kernels;
+    if (mr) allgather_ctl(h, CTL_CG_B, 2, s, kernels);
+  }
+  return kernels;
+}
+
+long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profile) {
+  long long kernels = 0;
+  const bool mr = multi(h);
+  const bool haveIf = h->nIfFaces > 0;
+  ldu_comm cm = h->comm;
+  for (int it = 0; it < batch; ++it) {
+    // the single fused reduction of the previous U (or init) runs on red_stream, overlapped
+    // with the SpMV below ("global synchronization can be overlapped by the sparse
+    // matrix-vector multiplication kernel")
+    if (mr) {
+      CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+      CUDA_CHECK(cudaStreamWaitEvent(h->red_stream, h->ev_fork, 0));
+      NCCL_CHECK(ncclAllGather(h->sums, h->gsums, kMaxVals, ncclDouble, cm->red, h->red_stream));
+      CUDA_CHECK(cudaEventRecord(h->ev_red, h->red_stream));
+      h->stats.allreduces++;
+    }
+    if (haveIf) {
+      k_pack<<<small_grid(h->nIfFaces), kBlock, 0, s>>>(h->nIfFaces, h->ifFaceCells, PACK_SCALED,
+                                                        h->w, h->rD, nullptr, nullptr, h->st,
+                                                        h->sendbuf);
+      ++kernels;
+      halo_exchange(h, s);
+    }
+    prof_mark(h, profile, 4 * it + 0, s);
+    with_format(h, [&](auto A) {
+      k_spmv_scaled<<<h->grid, kBlock, 0, s>>>(A, h->rD, h->w, h->nv, h->st);
+    });
+    prof_mark(h, profile, 4 * it + 1, s);
+    ++kernels;
+    if (haveIf) {
+      wait_halo(h, s);
+      k_iface_apply<<<small_grid(h->nIfCells), kBlock, 0, s>>>(
+          h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx, h->ifCoeffs, h->recvbuf, h->nv, h->st);
+      ++kernels;
+    }
+    if (mr) {
+      CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_red, 0));
+      k_ctl<<<1, 32, 0, s>>>(CTL_PIPE_NEXT, h->st, h->gsums, cm->nRanks, 3);
+      ++kernels;
+    }
+    // U: single rank runs the next top-of-iteration control in its last block
+    prof_mark(h, profile, 4 * it + 2, s);
+    k_pipe_U<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->nv, h->z, h->s, h->p0, h->x, h->r, h->w,
+                                        h->st, red_of(h, CTL_PIPE_NEXT, !mr));
+    prof_mark(h, profile, 4 * it + 3, s);
+    ++kernels;
+  }
+  return kernels;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// public-internal entry points
+// ---------------------------------------------------------------------------------------------
+void amul(ldu_handle h, const double* x, double* y) {
+  cudaStream_t s = h->own_stream;
+  long long kernels = 0;
+  h->stats = ldu_solve_stats{};
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, h->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_fork, 0));
+  }
+  const bool xd = is_device_ptr(x), yd = is_device_ptr(y);
+  const double* xin = x;
+  double* yout = y;
+  if (!xd) {
+    ensure_vec(h->bbuf, h->n);
+    CUDA_CHECK(cudaMemcpyAsync(h->bbuf, x, sizeof(double) * h->n, cudaMemcpyHostToDevice, s));
+    h->stats.h2dBytes += 8LL * h->n;
+    xin = h->bbuf;
+  }
+  if (!yd) {
+    ensure_vec(h->ybuf, h->n);
+    yout = h->ybuf;
+  }
+  amul_dev(h, xin, yout, s, kernels);
+  if (!yd) {
+    CUDA_CHECK(cudaMemcpyAsync(y, yout, sizeof(double) * h->n, cudaMemcpyDeviceToHost, s));
+    h->stats.d2hBytes += 8LL * h->n;
+  }
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+    CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_fork, 0));
+  }
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  h->stats.kernels = kernels;
+}
+
+ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, double tol,
+                 int maxIter, const ldu_solve_opts* opts, int* nIter, double* finalRes) {
+  if (!b || !x) fail_arg("b and x must not be NULL");
+  if (!(tol >= 0.0)) fail_arg("tol must be >= 0");
+  if (maxIter < 0) fail_arg("maxIter must be >= 0");
+  ldu_solve_opts o{};
+  if (opts) {
+    o = *opts;
+    for (int v : o.reserved)
+      if (v) fail_arg("ldu_solve_opts.reserved must be zero");
+  }
+  if (o.norm != LDU_NORM_L2 && o.norm != LDU_NORM_OPENFOAM) fail_arg("unknown norm");
+  if (o.batch < 0) fail_arg("batch must be >= 0");
+  if (o.profile != 0 && o.profile != 1) fail_arg("profile must be 0 or 1");
+  const bool profile = o.profile == 1;
+  const int batch = o.batch ? o.batch : 32;
+
+  ensure_work(h, pipelined);
+  const int n = h->n;
+  cudaStream_t s = h->own_stream;
+  const bool mr = multi(h);
+  h->stats = ldu_solve_stats{};
+  long long kernels = 0;
+
+  // order after the user's stream
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, h->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_fork, 0));
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev[0], s));
+
+  // inputs
+  const bool bd = is_device_ptr(b), xd = is_device_ptr(x);
+  const double* bin = b;
+  if (!bd) {
+    ensure_vec(h->bbuf, n);
+    CUDA_CHECK(cudaMemcpyAsync(h->bbuf, b, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    h->stats.h2dBytes += 8LL * n;
+    bin = h->bbuf;
+  }
+  CUDA_CHECK(cudaMemcpyAsync(h->x, x, sizeof(double) * n, xd ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  if (!xd) h->stats.h2dBytes += 8LL * n;
+
+  // history buffer
+  if (o.recordHistory) {
+    if (h->histCap < maxIter + 1) {
+      dfree(h->hist);
+      h->hist = nullptr;
+      h->histCap = 0;
+      h->hist = dmalloc<double>((size_t)maxIter + 1);
+      h->histCap = maxIter + 1;
+    }
+  }
+  h->histN = -1;
+
+  // state
+  State* sh = h->st_host;
+  std::memset(sh, 0, sizeof(State));
+  sh->tol = tol;
+  sh->maxIter = maxIter;
+  sh->norm = o.norm;
+  sh->record = o.recordHistory ? 1 : 0;
+  sh->hist = h->hist;
+  sh->histCap = h->histCap;
+  CUDA_CHECK(cudaMemcpyAsync(h->st, sh, sizeof(State), cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaMemsetAsync(h->ticket, 0, sizeof(unsigned), s));
+  if (pipelined) {
+    CUDA_CHECK(cudaMemsetAsync(h->z, 0, sizeof(double) * n, s));
+    CUDA_CHECK(cudaMemsetAsync(h->s, 0, sizeof(double) * n, s));
+    CUDA_CHECK(cudaMemsetAsync(h->p0, 0, sizeof(double) * n, s));
+  } else {
+    CUDA_CHECK(cudaMemsetAsync(h->p0, 0, sizeof(double) * n, s));
+    CUDA_CHECK(cudaMemsetAsync(h->p1, 0, sizeof(double) * n, s));
+  }
+
+  // ---- r0 = b - A x0 and the criterion scale ---------------------------------------------
+  double* sumA = pipelined ? h->nv : h->q;
+  if (o.norm == LDU_NORM_OPENFOAM) {
+    k_fill<<<small_grid(n), kBlock, 0, s>>>(n, 1.0, h->r);
+    ++kernels;
+    amul_dev(h, h->r, sumA, s, kernels);  // sumA = A 1 incl. interfaces
+    k_sum_x<<<h->grid, kBlock, 0, s>>>(n, h->x, h->st, red_of(h, CTL_XBAR, !mr));
+    ++kernels;
+    if (mr) allgather_ctl(h, CTL_XBAR, 2, s, kernels);
+  }
+  amul_dev(h, h->x, h->ybuf, s, kernels);
+  k_resid<<<h->grid, kBlock, 0, s>>>(n, bin, h->ybuf, sumA, h->rD, h->r, h->st,
+                                     red_of(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, !mr));
+  ++kernels;
+  if (mr) allgather_ctl(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, 3, s, kernels);
+  if (pipelined) {
+    // w0 = A u0 with u0 = rD.r0 (incl. interfaces), then the first fused reduction
+    if (h->nIfFaces) {
+      k_pack<<<small_grid(h->nIfFaces), kBlock, 0, s>>>(h->nIfFaces, h->ifFaceCells, PACK_SCALED,
+                                                        h->r, h->rD, nullptr, nullptr, h->st,
+                                                        h->sendbuf);
+      ++kernels;
+      halo_exchange(h, s);
+    }
+    with_format(h, [&](auto A) { k_spmv_scaled<<<h->grid, kBlock, 0, s>>>(A, h->rD, h->r, h->w, h->st); });
+    ++kernels;
+    if (h->nIfFaces) {
+      wait_halo(h, s);
+      k_iface_apply<<<small_grid(h->nIfCells), kBlock, 0, s>>>(
+          h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx, h->ifCoeffs, h->recvbuf, h->w, h->st);
+      ++kernels;
+    }
+    k_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->rD, h->r, h->w, h->st, red_of(h, CTL_PIPE_TOP, !mr));
+    ++kernels;
+    // multi-rank: the allgather of these sums is issued by the first loop trip (overlapped)
+  }
+  CUDA_CHECK(cudaGetLastError());
+  if (pipelined && mr) {
+    // k = -1 so that CTL_PIPE_NEXT of the first iteration evaluates i = 0
+    static const int minus_one = -1;
+    CUDA_CHECK(cudaMemcpyAsync(&h->st->k, &minus_one, sizeof(int), cudaMemcpyHostToDevice, s));
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev[1], s));
+
+  // ---- iteration batches as CUDA graphs ----------------------------------------------------
+  ldu_handle_s::Graph& G = h->graphs[pipelined ? 1 : 0][profile ? 1 : 0];
+  if (profile && (int)h->prof_ev.size() < 4 * batch) {
+    for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
+    h->prof_ev.assign(4 * batch, nullptr);
+    for (auto& e : h->prof_ev) CUDA_CHECK(cudaEventCreate(&e));
+    if (h->graphs[0][1].exec) { cudaGraphExecDestroy(h->graphs[0][1].exec); h->graphs[0][1] = {}; }
+    if (h->graphs[1][1].exec) { cudaGraphExecDestroy(h->graphs[1][1].exec); h->graphs[1][1] = {}; }
+  }
+  if (!G.exec || G.batch != batch) {
+    if (G.exec) {
+      cudaGraphExecDestroy(G.exec);
+      G = {};
+    }
+    const ldu_solve_stats saved = h->stats;  // capture enqueues nothing that runs now
+    cudaGraph_t g;
+    CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    G.kernels = pipelined ? enqueue_pipe_iters(h, batch, s, profile)
+                          : enqueue_cg_iters(h, batch, s, profile);
+    CUDA_CHECK(cudaStreamEndCapture(s, &g));
+    CUDA_CHECK(cudaGraphInstantiate(&G.exec, g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+    G.batch = batch;
+    h->stats = saved;
+  }
+  cudaGraphExec_t gexec = G.exec;
+  const long long kpb = G.kernels;
+  const long long redPerIter = mr ? (pipelined ? 1 : 2) : 0;
+  const long long haloPerIter = h->nIfFaces ? 8LL * h->nIfFaces : 0;
+  long long launched = 0;
+  int batches = 0;
+  std::vector<float> passT;  // profile: [batch][it][2] elapsed ms
+  // multi-rank pipelined needs one more loop trip: the decision on r_i is taken by the
+  // control kernel after the overlapped allgather of trip i (single rank: in U_{i-1}).
+  const long long trips = (long long)maxIter + ((pipelined && mr) ? 1 : 0);
+  auto collect = [&]() {
+    for (int it = 0; it < batch; ++it)
+      for (int p = 0; p < 2; ++p) {
+        float ms = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, h->prof_ev[4 * it + 2 * p], h->prof_ev[4 * it + 2 * p + 1]));
+        passT.push_back(ms);
+      }
+  };
+  if (maxIter > 0) {
+    if (tol == 0.0 && !profile) {  // fixed-iteration run: only breakdown / r == 0 stop early
+      const long long nb = (trips + batch - 1) / batch;
+      for (long long i = 0; i < nb; ++i) CUDA_CHECK(cudaGraphLaunch(gexec, s));
+      batches = (int)nb;
+    } else {
+      for (;;) {
+        CUDA_CHECK(cudaGraphLaunch(gexec, s));
+        ++batches;
+        CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        if (profile) collect();
+        if (sh->done) break;
+        if ((long long)batches * batch >= trips + batch) break;  // safety net
+      }
+    }
+  }
+  launched = (long long)batches * kpb;
+  h->stats.allreduces += (long long)batches * batch * redPerIter;
+  h->stats.haloBytes += (long long)batches * batch * haloPerIter;
+  CUDA_CHECK(cudaEventRecord(h->ev[2], s));
+
+  if (!pipelined) {
+    k_cg_final<<<small_grid(n), kBlock, 0, s>>>(n, h->p0, h->p1, h->x, h->st);
+    ++kernels;
+  }
+  CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  if (sh->zero_x) CUDA_CHECK(cudaMemsetAsync(h->x, 0, sizeof(double) * n, s));
+  CUDA_CHECK(cudaMemcpyAsync(x, h->x, sizeof(double) * n, xd ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if (!xd) h->stats.d2hBytes += 8LL * n;
+  CUDA_CHECK(cudaEventRecord(h->ev[3], s));
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+    CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_fork, 0));
+  }
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  CUDA_CHECK(cudaGetLastError());
+
+  float ms = 0.f;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[3]));
+  h->stats.solveMs = ms;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]));
+  h->stats.iterMs = ms;
+  h->stats.kernels = kernels + launched;
+  h->stats.iterations = sh->iter;
+  if (profile) {  // passes that did work: trips 0 .. iter-1 (multi-rank pipelined: 1 .. iter)
+    const long long first = (pipelined && mr) ? 1 : 0;
+    for (long long g = first; g < first + sh->iter && g < (long long)passT.size() / 2; ++g)
+      for (int p = 0; p < 2; ++p) {
+        h->stats.passMs[p] += passT[2 * g + p];
+        h->stats.passLaunches[p] += 1;
+      }
+  }
+  if (sh->record) h->histN = std::min(sh->iter + 1, h->histCap);
+  if (!sh->done) {  // safety net: batches exhausted without a decision
+    sh->status = LDU_NOT_CONVERGED;
+  }
+  if (nIter) *nIter = sh->iter;
+  if (finalRes) *finalRes = sh->res;
+  return (ldu_status)sh->status;
+}
+
+void release_work(ldu_handle h) {
+  for (double** p : {&h->x, &h->r, &h->p0, &h->p1, &h->q, &h->w, &h->nv, &h->z, &h->s,
+                     &h->bbuf, &h->ybuf, &h->hist}) {
+    dfree(*p);
+    *p = nullptr;
+  }
+  for (auto& row : h->graphs)
+    for (auto& G : row) {
+      if (G.exec) cudaGraphExecDestroy(G.exec);
+      G = {};
+    }
+  for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
+  h->prof_ev.clear();
+}
+
+// Launch geometry: grid = SMs x resident blocks of the heaviest pass (multiple of the SM count).
+void configure(ldu_handle h) {
+  cudaDeviceProp prop;
+  CUDA_CHECK(cudaGetDeviceProperties(&prop, h->device));
+  int occ = 1;
+  with_format(h, [&](auto A) {
+    using Fmt = decltype(A);
+    int o = 1;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_cg_passA<Fmt>, kBlock, 0));
+    occ = std::max(1, o);
+  });
+  long long need = ((long long)h->n + kBlock - 1) / kBlock;
+  long long g = (long long)prop.multiProcessorCount * occ;
+  if (need < g) g = need;
+  h->grid = (int)std::max(1LL, g);
+  h->maxParts = h->grid + 4096;
+  h->partials = dmalloc<double>((size_t)kMaxVals * h->maxParts);
+  h->ticket = dmalloc<unsigned>(1);
+  CUDA_CHECK(cudaMemset(h->ticket, 0, sizeof(unsigned)));
+  h->sums = dmalloc<double>(kMaxVals);
+  h->gsums = dmalloc<double>((size_t)kMaxVals * std::max(1, h->nRanks));
+  CUDA_CHECK(cudaMemset(h->gsums, 0, sizeof(double) * kMaxVals * std::max(1, h->nRanks)));
+  h->st = dmalloc<State>(1);
+  CUDA_CHECK(cudaMallocHost((void**)&h->st_host, sizeof(State)));
+}
+
+double stream_triad(int device, long long n, int reps) {
+  CUDA_CHECK(cudaSetDevice(device));
+  n &= ~1LL;
+  double *a = dmalloc<double>(n), *b = dmalloc<double>(n), *c = dmalloc<double>(n);
+  cudaStream_t s;
+  CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  CUDA_CHECK(cudaEventCreate(&e0));
+  CUDA_CHECK(cudaEventCreate(&e1));
+  CUDA_CHECK(cudaMemsetAsync(b, 0, 8 * n, s));
+  CUDA_CHECK(cudaMemsetAsync(c, 0, 8 * n, s));
+  cudaDeviceProp prop;
+  CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+  const int grid = prop.multiProcessorCount * 8;
+  double best = 0.0;
+  for (int r = 0; r < reps + 1; ++r) {
+    CUDA_CHECK(cudaEventRecord(e0, s));
+    k_triad<<<grid, 256, 0, s>>>(n, a, b, c, 3.0);
+    CUDA_CHECK(cudaEventRecord(e1, s));
+    CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    if (r > 0) best = std::max(best, 24.0 * n / (ms * 1e-3) / 1e9);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(s);
+  dfree(a);
+  dfree(b);
+  dfree(c);
+  return best;
+}
+
+}  // namespace ldu
