@@ -435,7 +435,9 @@ void ensure_work(ldu_handle h, bool pipelined) {
 
 // One batch of `batch` iterations, enqueued on s (captured into a graph by the caller).
 void prof_mark(ldu_handle h, bool profile, int idx, cudaStream_t s) {
-  if (profile) CUDA_CHECK(cudaEventRecord(h->prof_ev[idx], s));
+  // external event nodes: recorded by the graph on every launch (plain records inside a capture
+  // only express dependencies)
+  if (profile) CUDA_CHECK(cudaEventRecordWithFlags(h->prof_ev[idx], s, cudaEventRecordExternal));
 }
 
 long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile) {
