@@ -24,6 +24,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's version banner off stdout (one JSON line)
 
 METRIC = "CG iter/s & effective HBM GB/s, 256³ Poisson LDU, at 1/2/4/8 B200"
 UNIT = "iter/s"
@@ -359,7 +360,7 @@ def main():
                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": config_dict(args, world, info),
                "effective_gbps": value * bytes_iter / 1e9,
-               "effective_frac_of_hbm": value * bytes_iter / 1e9 / peak,
+               "effective_frac_of_hbm": value * bytes_iter / 1e9 / (peak * world),
                "bytes_per_iter_model": bytes_iter,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels,
                "clocks": clk, "last_status": int(st), "iterations_per_step": it}

@@ -140,7 +140,9 @@ struct ldu_handle_s {
   double* gsums = nullptr;     // [nRanks][kMaxVals]
   ldu::State* st = nullptr;
   ldu::State* st_host = nullptr;  // pinned
-  int grid = 0, block = ldu::kBlock;
+  int grid = 0, block = ldu::kBlock;  // streaming passes
+  int gridA = 0;                      // SpMV-bearing passes
+  int variant = 1;                    // DIA kernel variant (LDU_VARIANT)
   // history
   double* hist = nullptr;
   int histCap = 0;

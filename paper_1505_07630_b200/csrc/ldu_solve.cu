@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "ldu_dia.cuh"
 #include "ldu_kernels.cuh"
 
 namespace ldu {
@@ -194,6 +195,45 @@ __global__ void __launch_bounds__(kBlock) k_cg_passA(Fmt A, const double* __rest
   finish_reduction<1>(v, rd, st);
 }
 
+// classical pass A_k, DIA layout, all loads of ROWS rows hoisted (ldu_dia.cuh)
+template <int ND, int ROWS>
+__global__ void __launch_bounds__(kBlock) k_cg_passA_dia(DiaView<ND> A,
+                                                         const double* __restrict__ rD,
+                                                         const double* __restrict__ r, double* p0,
+                                                         double* p1, double* __restrict__ q,
+                                                         double* __restrict__ x, State* st, Red rd) {
+  if (st->done) return;
+  const int k = st->k;
+  const double beta = st->beta, alpha = st->alpha;
+  const double* __restrict__ pold = (k & 1) ? p0 : p1;
+  double* __restrict__ pnew = (k & 1) ? p1 : p0;
+  const OpCgP op{rD, r, pold, beta};
+  double v[1] = {0.0};
+  DIA_TILE_LOOP(base, A.n, ROWS) {
+    DiaRow<ND, OpCgP> row[ROWS];
+    double xc[ROWS];
+#pragma unroll
+    for (int u = 0; u < ROWS; ++u) {
+      const int c = (int)min(base + u * blockDim.x + threadIdx.x, (long long)A.n - 1);
+      row[u].load(A, op, c);
+      xc[u] = x[c];
+    }
+#pragma unroll
+    for (int u = 0; u < ROWS; ++u) {
+      const long long c = base + u * blockDim.x + threadIdx.x;
+      if (c < A.n) {
+        const double pc = op.eval(row[u].own);
+        const double qc = row[u].apply(op, pc / row[u].own[0]);
+        pnew[c] = pc;
+        q[c] = qc;
+        x[c] = fma(alpha, row[u].own[2], xc[u]);
+        v[0] = fma(pc, qc, v[0]);
+      }
+    }
+  }
+  finish_reduction<1>(v, rd, st);
+}
+
 // classical pass B_k
 __global__ void __launch_bounds__(kBlock) k_cg_passB(int n, const double* __restrict__ rD,
                                                      const double* __restrict__ q,
@@ -334,6 +374,75 @@ void with_format(ldu_handle h, F&& f) {
   }
 }
 
+template <class F>
+void with_dia(ldu_handle h, F&& f) {
+  auto dia = [&](auto tag) {
+    constexpr int ND = decltype(tag)::value;
+    DiaView<ND> v;
+    v.n = h->n;
+    for (int k = 0; k < ND; ++k) {
+      v.off[k] = h->off[k];
+      v.U[k] = h->U + (size_t)k * h->n;
+    }
+    f(v);
+  };
+  switch (h->nd) {
+    case 1: dia(std::integral_constant<int, 1>()); break;
+    case 2: dia(std::integral_constant<int, 2>()); break;
+    case 3: dia(std::integral_constant<int, 3>()); break;
+    case 4: dia(std::integral_constant<int, 4>()); break;
+    case 5: dia(std::integral_constant<int, 5>()); break;
+    case 6: dia(std::integral_constant<int, 6>()); break;
+    case 7: dia(std::integral_constant<int, 7>()); break;
+    case 8: dia(std::integral_constant<int, 8>()); break;
+    default: throw Error(LDU_ERR_STATE, "bad DIA offset count");
+  }
+}
+
+bool use_dia_kernels(ldu_handle h) { return h->layout == LDU_LAYOUT_DIA_SYM && h->variant > 0; }
+
+// y = A x over internal faces
+void launch_amul(ldu_handle h, const double* x, double* y, cudaStream_t s) {
+  if (use_dia_kernels(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if (h->variant == 2) k_amul_dia<ND, 2><<<h->gridA, kBlock, 0, s>>>(A, h->diag, x, y);
+      else k_amul_dia<ND, 1><<<h->gridA, kBlock, 0, s>>>(A, h->diag, x, y);
+    });
+  } else {
+    with_format(h, [&](auto A) { k_amul<<<h->gridA, kBlock, 0, s>>>(A, h->diag, x, y); });
+  }
+}
+
+// out = A (rD.in) over internal faces
+void launch_spmv_scaled(ldu_handle h, const double* in, double* out, cudaStream_t s) {
+  if (use_dia_kernels(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if (h->variant == 2) k_spmv_scaled_dia<ND, 2><<<h->gridA, kBlock, 0, s>>>(A, h->rD, in, out, h->st);
+      else k_spmv_scaled_dia<ND, 1><<<h->gridA, kBlock, 0, s>>>(A, h->rD, in, out, h->st);
+    });
+  } else {
+    with_format(h, [&](auto A) { k_spmv_scaled<<<h->gridA, kBlock, 0, s>>>(A, h->rD, in, out, h->st); });
+  }
+}
+
+void launch_passA(ldu_handle h, const Red& ra, cudaStream_t s) {
+  if (use_dia_kernels(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if (h->variant == 2)
+        k_cg_passA_dia<ND, 2><<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->r, h->p0, h->p1, h->q, h->x, h->st, ra);
+      else
+        k_cg_passA_dia<ND, 1><<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->r, h->p0, h->p1, h->q, h->x, h->st, ra);
+    });
+  } else {
+    with_format(h, [&](auto A) {
+      k_cg_passA<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->r, h->p0, h->p1, h->q, h->x, h->st, ra);
+    });
+  }
+}
+
 int small_grid(long long n) {
   long long b = (n + kBlock - 1) / kBlock;
   return (int)std::max(1LL, std::min(b, 4096LL));
@@ -345,7 +454,7 @@ struct Launch {
   cudaStream_t s;
 };
 
-Red red_of(ldu_handle h, int ctl, bool single) {
+Red red_of(ldu_handle h, int ctl, bool single, int grid = 0) {
   Red r;
   r.partials = h->partials;
   r.ld = h->maxParts;
@@ -353,7 +462,7 @@ Red red_of(ldu_handle h, int ctl, bool single) {
   r.sums = single ? h->gsums : h->sums;  // single rank: the local sums are the global sums
   r.ctl = single ? ctl : CTL_NONE;
   r.slot_base = 0;
-  r.total = h->grid;
+  r.total = grid ? grid : h->grid;
   r.store_only = 0;
   return r;
 }
@@ -401,7 +510,7 @@ void amul_dev(ldu_handle h, const double* x, double* y, cudaStream_t s, long lon
     ++kernels;
     halo_exchange(h, s);
   }
-  with_format(h, [&](auto A) { k_amul<<<h->grid, kBlock, 0, s>>>(A, h->diag, x, y); });
+  launch_amul(h, x, y, s);
   ++kernels;
   if (haveIf) {
     wait_halo(h, s);
@@ -453,20 +562,18 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
       ++kernels;
       halo_exchange(h, s);
     }
-    Red ra = red_of(h, CTL_CG_A, !mr);
+    Red ra = red_of(h, CTL_CG_A, !mr, h->gridA);
     if (haveIf) ra.store_only = 1;
     prof_mark(h, profile, 4 * it + 0, s);
-    with_format(h, [&](auto A) {
-      k_cg_passA<<<h->grid, kBlock, 0, s>>>(A, h->rD, h->r, h->p0, h->p1, h->q, h->x, h->st, ra);
-    });
+    launch_passA(h, ra, s);
     prof_mark(h, profile, 4 * it + 1, s);
     ++kernels;
     if (haveIf) {
       wait_halo(h, s);
       Red ri = red_of(h, CTL_CG_A, !mr);
-      const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->grid);
-      ri.slot_base = h->grid;
-      ri.total = h->grid + ig;
+      const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->gridA);
+      ri.slot_base = h->gridA;
+      ri.total = h->gridA + ig;
       k_iface_cg<<<ig, kBlock, 0, s>>>(h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx,
                                        h->ifCoeffs, h->recvbuf, h->q, h->p0, h->p1, h->st, ri);
       ++kernels;
@@ -506,9 +613,7 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
       halo_exchange(h, s);
     }
     prof_mark(h, profile, 4 * it + 0, s);
-    with_format(h, [&](auto A) {
-      k_spmv_scaled<<<h->grid, kBlock, 0, s>>>(A, h->rD, h->w, h->nv, h->st);
-    });
+    launch_spmv_scaled(h, h->w, h->nv, s);
     prof_mark(h, profile, 4 * it + 1, s);
     ++kernels;
     if (haveIf) {
@@ -671,7 +776,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
       ++kernels;
       halo_exchange(h, s);
     }
-    with_format(h, [&](auto A) { k_spmv_scaled<<<h->grid, kBlock, 0, s>>>(A, h->rD, h->r, h->w, h->st); });
+    launch_spmv_scaled(h, h->r, h->w, s);
     ++kernels;
     if (h->nIfFaces) {
       wait_halo(h, s);
@@ -816,18 +921,31 @@ void release_work(ldu_handle h) {
 void configure(ldu_handle h) {
   cudaDeviceProp prop;
   CUDA_CHECK(cudaGetDeviceProperties(&prop, h->device));
-  int occ = 1;
-  with_format(h, [&](auto A) {
-    using Fmt = decltype(A);
+  // kernel variant of the SpMV-bearing passes (DIA layout): 0 generic, 1 hoisted, 2 hoisted x2
+  h->variant = 0;
+  if (const char* v = std::getenv("LDU_VARIANT")) h->variant = std::atoi(v);
+  if (h->variant < 0 || h->variant > 2) h->variant = 0;
+  const long long need = ((long long)h->n + kBlock - 1) / kBlock;
+  auto grid_of = [&](const void* fn) {
     int o = 1;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_cg_passA<Fmt>, kBlock, 0));
-    occ = std::max(1, o);
-  });
-  long long need = ((long long)h->n + kBlock - 1) / kBlock;
-  long long g = (long long)prop.multiProcessorCount * occ;
-  if (need < g) g = need;
-  h->grid = (int)std::max(1LL, g);
-  h->maxParts = h->grid + 4096;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kBlock, 0));
+    long long g = (long long)prop.multiProcessorCount * std::max(1, o);
+    return (int)std::max(1LL, std::min(g, need));
+  };
+  h->grid = grid_of((const void*)k_cg_passB);  // streaming passes
+  if (use_dia_kernels(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      h->gridA = h->variant == 2 ? grid_of((const void*)k_cg_passA_dia<ND, 2>)
+                                 : grid_of((const void*)k_cg_passA_dia<ND, 1>);
+    });
+  } else {
+    with_format(h, [&](auto A) {
+      using Fmt = decltype(A);
+      h->gridA = grid_of((const void*)k_cg_passA<Fmt>);
+    });
+  }
+  h->maxParts = std::max(h->grid, h->gridA) + 4096;
   h->partials = dmalloc<double>((size_t)kMaxVals * h->maxParts);
   h->ticket = dmalloc<unsigned>(1);
   CUDA_CHECK(cudaMemset(h->ticket, 0, sizeof(unsigned)));

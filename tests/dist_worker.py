@@ -1,0 +1,93 @@
+"""Multi-rank worker for the distributed parity test (launched by torchrun, one rank per GPU).
+
+Every rank builds the same global system, takes its contiguous slab (meshgen.slab_partition),
+sets up the NCCL comm (unique id broadcast over torch.distributed), and runs ldu_amul, pcg_solve
+and pipecg_solve through the C ABI.  Rank 0 gathers the slabs and compares with the CPU oracle on
+the global system.  Prints "DIST_OK <json>" on success; exits non-zero on failure.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import meshgen  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1505_07630_b200 as ldu
+
+    uid = [ldu.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = ldu.Comm(rank, world, uid[0], local)
+    results = {}
+    cases = {
+        "hex": lambda: meshgen.hex_laplacian(24, 20, 32, dirichlet=dict(x0=1.0)),
+        "hex_sigma": lambda: meshgen.hex_laplacian(17, 13, 19, conductance_sigma=0.8, seed=3,
+                                                   dirichlet=dict(x0=1.0)),
+        "irregular": lambda: meshgen.irregular_mesh(14, seed=7),
+    }
+    ok = True
+    for name, mk in cases.items():
+        g = mk()
+        parts = meshgen.slab_partition(g, world)
+        me = parts[rank]
+        bounds = meshgen.slab_bounds(g.nCells, world)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        A = ldu.LduMatrix.from_system(me, comm)
+        xg = np.random.default_rng(5).uniform(-1, 1, g.nCells)
+        y = torch.empty(me.nCells, dtype=torch.float64, device="cuda")
+        A.amul(torch.from_numpy(xg[lo:hi].copy()).cuda(), y)
+        out = {"amul": y.cpu().numpy()}
+        b = torch.from_numpy(g.b[lo:hi].copy()).cuda()
+        for solver in ("pcg", "pipecg"):
+            x = torch.zeros_like(b)
+            fn = A.pcg_solve if solver == "pcg" else A.pipecg_solve
+            st, it, res = fn(b, x, tol=1e-10, maxIter=5000)
+            stats = A.stats()
+            out[solver] = (st, it, res, x.cpu().numpy(), stats["allreduces"])
+        A.close()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, out)
+        if rank == 0:
+            import oracle
+            y_all = np.concatenate([o["amul"] for o in gathered])
+            yo = oracle.amul(g, xg)
+            r = {"amul_rel": float(np.linalg.norm(y_all - yo) / np.linalg.norm(yo))}
+            ok &= r["amul_rel"] <= 1e-12
+            for solver in ("pcg", "pipecg"):
+                ofn = oracle.pcg if solver == "pcg" else oracle.pipecg
+                ost, ox, oit, ores = ofn(g, g.b, tol=1e-10, maxIter=5000)
+                sts = {o[solver][0] for o in gathered}
+                its = {o[solver][1] for o in gathered}
+                x_all = np.concatenate([o[solver][3] for o in gathered])
+                rel = float(np.linalg.norm(x_all - ox) / np.linalg.norm(ox))
+                it = gathered[0][solver][1]
+                reds = gathered[0][solver][4]
+                r[solver] = dict(status=sorted(sts), iters=sorted(its), oracle_iters=oit,
+                                 rel=rel, allreduces=reds)
+                ok &= sts == {0} and len(its) == 1 and abs(it - oit) <= max(1, round(0.02 * oit))
+                ok &= rel <= 1e-8
+                per_iter = 2 if solver == "pcg" else 1  # reading Z4 / P:97
+                ok &= reds >= per_iter * it
+            results[name] = r
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(("DIST_OK " if ok else "DIST_FAIL ") + json.dumps(results), flush=True)
+        sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
