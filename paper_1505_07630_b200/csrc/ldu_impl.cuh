@@ -142,7 +142,10 @@ struct ldu_handle_s {
   ldu::State* st_host = nullptr;  // pinned
   int grid = 0, block = ldu::kBlock;  // streaming passes
   int gridA = 0;                      // SpMV-bearing passes
-  int variant = 1;                    // DIA kernel variant (LDU_VARIANT)
+  int variant = 0;                    // DIA kernel variant (LDU_VARIANT)
+  bool marchOk = false;               // plane-marching geometry applies
+  bool marchStrict = false;           // ... with the performance geometry (one wave, lockstep)
+  int mT = 0, mH = 0, mTiles = 0, mPlanes = 0, mChunk = 0;
   // history
   double* hist = nullptr;
   int histCap = 0;

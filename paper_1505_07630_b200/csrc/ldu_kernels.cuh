@@ -234,20 +234,31 @@ __device__ __forceinline__ void run_ctl(int ctl, State* st, const double* s) {
   }
 }
 
-// Common epilogue: partials -> (last block) local sums -> (single rank) control step.
-struct RedArgs {
+struct Red {  // reduction plumbing of one pass
   double* partials;
   int ld;
   unsigned* ticket;
-  double* sums;  // local sums (send buffer of the cross-rank allgather)
-  int ctl;       // control step to run here when single-rank, else CTL_NONE
+  double* sums;
+  int ctl;         // control step run by the last block (single rank) or CTL_NONE
+  int slot_base;   // first partial slot of this kernel
+  int total;       // slots summed by the last block
+  int store_only;  // 1: store partials only (a later kernel finishes the reduction)
 };
 
 template <int NV>
-__device__ __forceinline__ void epilogue(double (&v)[NV], const RedArgs& ra, State* st) {
-  if (store_partial_is_last<NV>(v, ra.partials, ra.ld, blockIdx.x, ra.ticket, gridDim.x)) {
-    sum_partials<NV>(ra.partials, ra.ld, gridDim.x, ra.sums, ra.ticket);
-    if (threadIdx.x == 0 && ra.ctl != CTL_NONE) run_ctl(ra.ctl, st, ra.sums);
+__device__ __forceinline__ void finish_reduction(double (&v)[NV], const Red& rd, State* st) {
+  if (rd.store_only) {
+    __shared__ double sm[NV][32];
+    block_reduce<NV>(v, sm);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) rd.partials[k * rd.ld + rd.slot_base + blockIdx.x] = v[k];
+    return;
+  }
+  if (store_partial_is_last<NV>(v, rd.partials, rd.ld, rd.slot_base + blockIdx.x, rd.ticket,
+                                gridDim.x)) {
+    sum_partials<NV>(rd.partials, rd.ld, rd.total, rd.sums, rd.ticket);
+    if (threadIdx.x == 0 && rd.ctl != CTL_NONE) run_ctl(rd.ctl, st, rd.sums);
   }
 }
 

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "ldu_dia.cuh"
+#include "ldu_march.cuh"
 #include "ldu_kernels.cuh"
 
 namespace ldu {
@@ -30,34 +31,6 @@ namespace {
 // ---------------------------------------------------------------------------------------------
 #define GRID_STRIDE(c, n) \
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < (n); c += gridDim.x * blockDim.x)
-
-struct Red {  // reduction plumbing of one pass
-  double* partials;
-  int ld;
-  unsigned* ticket;
-  double* sums;
-  int ctl;         // control step run by the last block (single rank) or CTL_NONE
-  int slot_base;   // first partial slot of this kernel
-  int total;       // slots summed by the last block
-  int store_only;  // 1: store partials only (a later kernel finishes the reduction)
-};
-
-template <int NV>
-__device__ __forceinline__ void finish_reduction(double (&v)[NV], const Red& rd, State* st) {
-  if (rd.store_only) {
-    __shared__ double sm[NV][32];
-    block_reduce<NV>(v, sm);
-    if (threadIdx.x == 0)
-#pragma unroll
-      for (int k = 0; k < NV; ++k) rd.partials[k * rd.ld + rd.slot_base + blockIdx.x] = v[k];
-    return;
-  }
-  if (store_partial_is_last<NV>(v, rd.partials, rd.ld, rd.slot_base + blockIdx.x, rd.ticket,
-                                gridDim.x)) {
-    sum_partials<NV>(rd.partials, rd.ld, rd.total, rd.sums, rd.ticket);
-    if (threadIdx.x == 0 && rd.ctl != CTL_NONE) run_ctl(rd.ctl, st, rd.sums);
-  }
-}
 
 // y = A x over internal faces (diag first, ascending columns).
 template <class Fmt>
@@ -399,11 +372,35 @@ void with_dia(ldu_handle h, F&& f) {
   }
 }
 
-bool use_dia_kernels(ldu_handle h) { return h->layout == LDU_LAYOUT_DIA_SYM && h->variant > 0; }
+bool use_dia_kernels(ldu_handle h) {
+  return h->layout == LDU_LAYOUT_DIA_SYM && (h->variant == 1 || h->variant == 2);
+}
+bool use_march(ldu_handle h) { return h->layout == LDU_LAYOUT_DIA_SYM && h->variant == 3 && h->marchOk; }
+
+template <int ND, int MODE>
+MarchArgs<ND, MODE> march_args(ldu_handle h, const DiaView<ND>& A) {
+  MarchArgs<ND, MODE> a{};
+  a.A = A;
+  a.g = MarchGeom{h->mT, h->mH, h->mTiles, h->mPlanes, h->mChunk};
+  return a;
+}
+
+size_t march_smem(ldu_handle h) { return sizeof(double) * 3 * (size_t)(h->mT + 2 * h->mH); }
 
 // y = A x over internal faces
 void launch_amul(ldu_handle h, const double* x, double* y, cudaStream_t s) {
-  if (use_dia_kernels(h)) {
+  if (use_march(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if constexpr (ND >= 2) {
+        auto a = march_args<ND, MARCH_AMUL>(h, A);
+        a.in0 = x;
+        a.diag = h->diag;
+        a.out = y;
+        k_march<ND, MARCH_AMUL><<<h->gridA, kBlock, march_smem(h), s>>>(a, h->st, Red{});
+      }
+    });
+  } else if (use_dia_kernels(h)) {
     with_dia(h, [&](auto A) {
       constexpr int ND = sizeof(A.off) / sizeof(int);
       if (h->variant == 2) k_amul_dia<ND, 2><<<h->gridA, kBlock, 0, s>>>(A, h->diag, x, y);
@@ -416,7 +413,18 @@ void launch_amul(ldu_handle h, const double* x, double* y, cudaStream_t s) {
 
 // out = A (rD.in) over internal faces
 void launch_spmv_scaled(ldu_handle h, const double* in, double* out, cudaStream_t s) {
-  if (use_dia_kernels(h)) {
+  if (use_march(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if constexpr (ND >= 2) {
+        auto a = march_args<ND, MARCH_S>(h, A);
+        a.in0 = h->rD;
+        a.in1 = in;
+        a.out = out;
+        k_march<ND, MARCH_S><<<h->gridA, kBlock, march_smem(h), s>>>(a, h->st, Red{});
+      }
+    });
+  } else if (use_dia_kernels(h)) {
     with_dia(h, [&](auto A) {
       constexpr int ND = sizeof(A.off) / sizeof(int);
       if (h->variant == 2) k_spmv_scaled_dia<ND, 2><<<h->gridA, kBlock, 0, s>>>(A, h->rD, in, out, h->st);
@@ -428,7 +436,21 @@ void launch_spmv_scaled(ldu_handle h, const double* in, double* out, cudaStream_
 }
 
 void launch_passA(ldu_handle h, const Red& ra, cudaStream_t s) {
-  if (use_dia_kernels(h)) {
+  if (use_march(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if constexpr (ND >= 2) {
+        auto a = march_args<ND, MARCH_A>(h, A);
+        a.in0 = h->rD;
+        a.in1 = h->r;
+        a.p0 = h->p0;
+        a.p1 = h->p1;
+        a.out = h->q;
+        a.x = h->x;
+        k_march<ND, MARCH_A><<<h->gridA, kBlock, march_smem(h), s>>>(a, h->st, ra);
+      }
+    });
+  } else if (use_dia_kernels(h)) {
     with_dia(h, [&](auto A) {
       constexpr int ND = sizeof(A.off) / sizeof(int);
       if (h->variant == 2)
@@ -924,7 +946,7 @@ void configure(ldu_handle h) {
   // kernel variant of the SpMV-bearing passes (DIA layout): 0 generic, 1 hoisted, 2 hoisted x2
   h->variant = 0;
   if (const char* v = std::getenv("LDU_VARIANT")) h->variant = std::atoi(v);
-  if (h->variant < 0 || h->variant > 2) h->variant = 0;
+  if (h->variant < 0 || h->variant > 3) h->variant = 0;
   const long long need = ((long long)h->n + kBlock - 1) / kBlock;
   auto grid_of = [&](const void* fn) {
     int o = 1;
@@ -933,7 +955,62 @@ void configure(ldu_handle h) {
     return (int)std::max(1LL, std::min(g, need));
   };
   h->grid = grid_of((const void*)k_cg_passB);  // streaming passes
-  if (use_dia_kernels(h)) {
+  // plane-marching geometry (DIA with one far offset D >= 4096 and near offsets <= 1024)
+  h->marchOk = false;
+  if (h->layout == LDU_LAYOUT_DIA_SYM && h->nd >= 2) {
+    const int D = h->off[h->nd - 1], H = h->off[h->nd - 2];
+    if (D >= 4096 && H <= kMarchHMax && H < D) {
+      h->marchOk = true;
+      h->mT = kMarchT;
+      h->mH = H;
+      h->mTiles = (D + h->mT - 1) / h->mT;
+      h->mPlanes = (int)(((long long)h->n + D - 1) / D);
+    }
+  }
+  if (h->variant == 3 && !h->marchOk) h->variant = 0;
+  if (use_march(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if constexpr (ND >= 2) {
+        const size_t smem = march_smem(h);
+        const void* fns[3] = {(const void*)k_march<ND, MARCH_AMUL>, (const void*)k_march<ND, MARCH_S>,
+                              (const void*)k_march<ND, MARCH_A>};
+        int occ = 1 << 30;
+        for (const void* fn : fns) {
+          CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          int o = 1;
+          CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kBlock, smem));
+          occ = std::min(occ, std::max(1, o));
+        }
+        // grid G = SMs * occ = tiles * chunks; the tile width T = ceil(D / tiles) <= kMarchT.
+        // Largest chunk count (most parallel planes) keeping T <= kMarchT and >= 2H, and at
+        // least 8 planes per chunk (prologue of 2 planes per chunk).
+        const int D = h->off[h->nd - 1];
+        const long long G = (long long)prop.multiProcessorCount * occ;
+        int bestTiles = 0, bestCh = 0;
+        for (long long ch = 1; ch <= G; ++ch) {
+          if (G % ch) continue;
+          const long long tiles = G / ch;
+          const long long T = (D + tiles - 1) / tiles;
+          if (T > kMarchT || T < 2LL * h->mH || T < kBlock) continue;
+          if ((h->mPlanes + ch - 1) / ch < 8) continue;
+          bestTiles = (int)tiles;
+          bestCh = (int)ch;  // keep the largest ch (ascending loop)
+        }
+        h->marchStrict = bestTiles > 0;
+        if (!bestTiles) {  // relaxed geometry (small meshes; only used when LDU_VARIANT=3)
+          long long T = std::max<long long>({(D + G - 1) / G, 2LL * h->mH, 32LL});
+          T = std::min<long long>(T, kMarchT);
+          bestTiles = (int)((D + T - 1) / T);
+          bestCh = (int)std::max(1LL, std::min<long long>(h->mPlanes, G / bestTiles));
+        }
+        h->mTiles = bestTiles;
+        h->mT = (D + bestTiles - 1) / bestTiles;
+        h->mChunk = (h->mPlanes + bestCh - 1) / bestCh;
+        h->gridA = bestTiles * ((h->mPlanes + h->mChunk - 1) / h->mChunk);
+      }
+    });
+  } else if (use_dia_kernels(h)) {
     with_dia(h, [&](auto A) {
       constexpr int ND = sizeof(A.off) / sizeof(int);
       h->gridA = h->variant == 2 ? grid_of((const void*)k_cg_passA_dia<ND, 2>)
