@@ -146,6 +146,9 @@ struct ldu_handle_s {
   bool marchOk = false;               // plane-marching geometry applies
   bool marchStrict = false;           // ... with the performance geometry (one wave, lockstep)
   int mT = 0, mH = 0, mTiles = 0, mPlanes = 0, mChunk = 0;
+  bool tmaOk = false, tmaStrict = false;  // TMA plane march (variant 4)
+  int tT = 0, tTiles = 0, tChunk = 0, tGrid = 0, tL = 1;
+  int chunkK = 2048;                  // variant 5: rows per chunk
   // history
   double* hist = nullptr;
   int histCap = 0;

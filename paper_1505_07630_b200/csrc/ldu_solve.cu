@@ -20,6 +20,7 @@
 
 #include "ldu_dia.cuh"
 #include "ldu_march.cuh"
+#include "ldu_tma.cuh"
 #include "ldu_kernels.cuh"
 
 namespace ldu {
@@ -166,6 +167,53 @@ __global__ void __launch_bounds__(kBlock) k_cg_passA(Fmt A, const double* __rest
     v[0] = fma(pc, qc, v[0]);
   }
   finish_reduction<1>(v, rd, st);
+}
+
+// classical pass A_k, chunked wavefront: block b walks chunks b, b + G, ... of K consecutive rows,
+// 256 rows at a time, so the +-nx gathers of a tile were loaded by the same block one tile
+// earlier (L1 hits) while whole chunks still advance as a wavefront (+-nx*ny gathers in L2).
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_cg_passA_chunk(Fmt A, const double* __restrict__ rD,
+                                                           const double* __restrict__ r, double* p0,
+                                                           double* p1, double* __restrict__ q,
+                                                           double* __restrict__ x, State* st, Red rd,
+                                                           int K) {
+  if (st->done) return;
+  const int k = st->k;
+  const double beta = st->beta, alpha = st->alpha;
+  const double* __restrict__ pold = (k & 1) ? p0 : p1;
+  double* __restrict__ pnew = (k & 1) ? p1 : p0;
+  double v[1] = {0.0};
+  const int nchunks = (A.n + K - 1) / K;
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int end = min(A.n, (ch + 1) * K);
+    for (int c = ch * K + threadIdx.x; c < end; c += kBlock) {
+      auto op = [&](int j) { return fma(beta, __ldg(pold + j), __ldg(rD + j) * __ldg(r + j)); };
+      const double po = __ldg(pold + c);
+      const double pc = fma(beta, po, __ldg(rD + c) * __ldg(r + c));
+      const double qc = row_apply(A, c, pc / __ldg(rD + c), op);
+      pnew[c] = pc;
+      q[c] = qc;
+      x[c] = fma(alpha, po, x[c]);
+      v[0] = fma(pc, qc, v[0]);
+    }
+  }
+  finish_reduction<1>(v, rd, st);
+}
+
+// out = A (rD.in), chunked wavefront (see k_cg_passA_chunk)
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_spmv_scaled_chunk(Fmt A, const double* __restrict__ rD,
+                                                              const double* __restrict__ in,
+                                                              double* __restrict__ out,
+                                                              const State* st, int K) {
+  if (st->done) return;
+  const int nchunks = (A.n + K - 1) / K;
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int end = min(A.n, (ch + 1) * K);
+    for (int c = ch * K + threadIdx.x; c < end; c += kBlock)
+      out[c] = row_apply(A, c, __ldg(in + c), [&](int j) { return __ldg(rD + j) * __ldg(in + j); });
+  }
 }
 
 // classical pass A_k, DIA layout, all loads of ROWS rows hoisted (ldu_dia.cuh)
@@ -376,6 +424,29 @@ bool use_dia_kernels(ldu_handle h) {
   return h->layout == LDU_LAYOUT_DIA_SYM && (h->variant == 1 || h->variant == 2);
 }
 bool use_march(ldu_handle h) { return h->layout == LDU_LAYOUT_DIA_SYM && h->variant == 3 && h->marchOk; }
+bool use_tma(ldu_handle h) { return h->layout == LDU_LAYOUT_DIA_SYM && h->variant == 4 && h->tmaOk; }
+
+template <int ND, int MODE>
+size_t tma_smem(ldu_handle h) {
+  return sizeof(double) * (size_t)(h->tL == 1 ? tma_smem_doubles<ND, MODE, 1>(h->tT, h->mH)
+                                              : tma_smem_doubles<ND, MODE, 2>(h->tT, h->mH));
+}
+
+template <int ND, int MODE>
+void launch_tma(ldu_handle h, const MarchArgs<ND, MODE>& a, const Red& rd, cudaStream_t s) {
+  if (h->tL == 1)
+    k_tma_march<ND, MODE, 1><<<h->tGrid, kTmaThreads, tma_smem<ND, MODE>(h), s>>>(a, h->st, rd);
+  else
+    k_tma_march<ND, MODE, 2><<<h->tGrid, kTmaThreads, tma_smem<ND, MODE>(h), s>>>(a, h->st, rd);
+}
+
+template <int ND, int MODE>
+MarchArgs<ND, MODE> tma_args(ldu_handle h, const DiaView<ND>& A) {
+  MarchArgs<ND, MODE> a{};
+  a.A = A;
+  a.g = MarchGeom{h->tT, h->mH, h->tTiles, h->mPlanes, h->tChunk};
+  return a;
+}
 
 template <int ND, int MODE>
 MarchArgs<ND, MODE> march_args(ldu_handle h, const DiaView<ND>& A) {
@@ -389,7 +460,18 @@ size_t march_smem(ldu_handle h) { return sizeof(double) * 3 * (size_t)(h->mT + 2
 
 // y = A x over internal faces
 void launch_amul(ldu_handle h, const double* x, double* y, cudaStream_t s) {
-  if (use_march(h)) {
+  if (use_tma(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if constexpr (ND >= 2) {
+        auto a = tma_args<ND, MARCH_AMUL>(h, A);
+        a.in0 = x;
+        a.diag = h->diag;
+        a.out = y;
+        launch_tma<ND, MARCH_AMUL>(h, a, Red{}, s);
+      }
+    });
+  } else if (use_march(h)) {
     with_dia(h, [&](auto A) {
       constexpr int ND = sizeof(A.off) / sizeof(int);
       if constexpr (ND >= 2) {
@@ -413,7 +495,22 @@ void launch_amul(ldu_handle h, const double* x, double* y, cudaStream_t s) {
 
 // out = A (rD.in) over internal faces
 void launch_spmv_scaled(ldu_handle h, const double* in, double* out, cudaStream_t s) {
-  if (use_march(h)) {
+  if (h->variant == 5) {
+    with_format(h, [&](auto A) {
+      k_spmv_scaled_chunk<<<h->gridA, kBlock, 0, s>>>(A, h->rD, in, out, h->st, h->chunkK);
+    });
+  } else if (use_tma(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if constexpr (ND >= 2) {
+        auto a = tma_args<ND, MARCH_S>(h, A);
+        a.in0 = h->rD;
+        a.in1 = in;
+        a.out = out;
+        launch_tma<ND, MARCH_S>(h, a, Red{}, s);
+      }
+    });
+  } else if (use_march(h)) {
     with_dia(h, [&](auto A) {
       constexpr int ND = sizeof(A.off) / sizeof(int);
       if constexpr (ND >= 2) {
@@ -436,7 +533,26 @@ void launch_spmv_scaled(ldu_handle h, const double* in, double* out, cudaStream_
 }
 
 void launch_passA(ldu_handle h, const Red& ra, cudaStream_t s) {
-  if (use_march(h)) {
+  if (h->variant == 5) {
+    with_format(h, [&](auto A) {
+      k_cg_passA_chunk<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->r, h->p0, h->p1, h->q, h->x, h->st, ra,
+                                                   h->chunkK);
+    });
+  } else if (use_tma(h)) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if constexpr (ND >= 2) {
+        auto a = tma_args<ND, MARCH_A>(h, A);
+        a.in0 = h->rD;
+        a.in1 = h->r;
+        a.p0 = h->p0;
+        a.p1 = h->p1;
+        a.out = h->q;
+        a.x = h->x;
+        launch_tma<ND, MARCH_A>(h, a, ra, s);
+      }
+    });
+  } else if (use_march(h)) {
     with_dia(h, [&](auto A) {
       constexpr int ND = sizeof(A.off) / sizeof(int);
       if constexpr (ND >= 2) {
@@ -946,7 +1062,9 @@ void configure(ldu_handle h) {
   // kernel variant of the SpMV-bearing passes (DIA layout): 0 generic, 1 hoisted, 2 hoisted x2
   h->variant = 0;
   if (const char* v = std::getenv("LDU_VARIANT")) h->variant = std::atoi(v);
-  if (h->variant < 0 || h->variant > 3) h->variant = 0;
+  if (h->variant < 0 || h->variant > 5) h->variant = 0;
+  h->chunkK = 2048;
+  if (const char* v = std::getenv("LDU_CHUNK")) h->chunkK = std::max(256, std::atoi(v) / 256 * 256);
   const long long need = ((long long)h->n + kBlock - 1) / kBlock;
   auto grid_of = [&](const void* fn) {
     int o = 1;
@@ -967,6 +1085,56 @@ void configure(ldu_handle h) {
       h->mPlanes = (int)(((long long)h->n + D - 1) / D);
     }
   }
+  // TMA plane march: one 512-thread block per SM, grid = tiles * chunks = #SMs, T even and
+  // small enough that the shared footprint of the heaviest mode fits; D, H, n even (16 B copies)
+  h->tmaOk = false;
+  h->tL = 1;
+  if (const char* v = std::getenv("LDU_TMA_L")) h->tL = std::atoi(v) == 2 ? 2 : 1;
+  if (h->marchOk && h->off[h->nd - 1] % 2 == 0 && h->mH % 2 == 0 && h->n % 2 == 0) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      if constexpr (ND >= 2) {
+        const int D = h->off[h->nd - 1];
+        const long long G = prop.multiProcessorCount;
+        const long long maxSmem = prop.sharedMemPerBlockOptin - 2048;  // static smem headroom
+        int bestTiles = 0, bestCh = 0;
+        long long bestT = 0;
+        bool bestStrict = false;
+        for (long long ch = 1; ch <= G; ++ch) {
+          if (G % ch) continue;
+          const long long tiles = G / ch;
+          long long T = (D + tiles - 1) / tiles;
+          T += T & 1;
+          const long long need = h->tL == 1 ? tma_smem_doubles<ND, MARCH_A, 1>(T, h->mH)
+                                            : tma_smem_doubles<ND, MARCH_A, 2>(T, h->mH);
+          if (8LL * need > maxSmem) continue;
+          const bool strict = T >= 2LL * h->mH && T >= 256 && (h->mPlanes + ch - 1) / ch >= 8;
+          // prefer strict geometries, then the largest tile (least halo re-read)
+          if (!bestTiles || (strict && !bestStrict) || (strict == bestStrict && T > bestT)) {
+            bestTiles = (int)tiles;
+            bestCh = (int)ch;
+            bestT = T;
+            bestStrict = strict;
+          }
+        }
+        if (bestTiles) {
+          h->tmaOk = true;
+          h->tmaStrict = bestStrict;
+          h->tT = (int)bestT;
+          h->tTiles = bestTiles;
+          h->tChunk = (h->mPlanes + bestCh - 1) / bestCh;
+          h->tGrid = bestTiles * ((h->mPlanes + h->tChunk - 1) / h->tChunk);
+          const void* fns[6] = {(const void*)k_tma_march<ND, MARCH_AMUL, 1>, (const void*)k_tma_march<ND, MARCH_S, 1>,
+                                (const void*)k_tma_march<ND, MARCH_A, 1>, (const void*)k_tma_march<ND, MARCH_AMUL, 2>,
+                                (const void*)k_tma_march<ND, MARCH_S, 2>, (const void*)k_tma_march<ND, MARCH_A, 2>};
+          const size_t sm[3] = {tma_smem<ND, MARCH_AMUL>(h), tma_smem<ND, MARCH_S>(h), tma_smem<ND, MARCH_A>(h)};
+          for (int i = 0; i < 6; ++i)
+            CUDA_CHECK(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm[i % 3]));
+        }
+      }
+    });
+  }
+  if (h->variant == 4 && !h->tmaOk) h->variant = 0;
   if (h->variant == 3 && !h->marchOk) h->variant = 0;
   if (use_march(h)) {
     with_dia(h, [&](auto A) {
@@ -1020,6 +1188,16 @@ void configure(ldu_handle h) {
     with_format(h, [&](auto A) {
       using Fmt = decltype(A);
       h->gridA = grid_of((const void*)k_cg_passA<Fmt>);
+    });
+  }
+  if (use_tma(h)) h->gridA = h->tGrid;
+  if (h->variant == 5) {
+    with_format(h, [&](auto A) {
+      using Fmt = decltype(A);
+      const void* fns[2] = {(const void*)k_cg_passA_chunk<Fmt>, (const void*)k_spmv_scaled_chunk<Fmt>};
+      for (const void* fn : fns)  // all of the unified L1/shared storage as L1
+        CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+      h->gridA = grid_of((const void*)k_cg_passA_chunk<Fmt>);
     });
   }
   h->maxParts = std::max(h->grid, h->gridA) + 4096;
