@@ -37,7 +37,9 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--solver", default="pcg", choices=["pcg", "pipecg"])
+    p.add_argument("--solver", default="pipecg", choices=["pcg", "pipecg"],
+                   help="headline solver; the other one is measured too (key 'secondary')")
+    p.add_argument("--no-secondary", action="store_true")
     p.add_argument("--n", type=int, default=256, help="mesh is n^3 (config 3: 256)")
     p.add_argument("--iters", type=int, default=200, help="fixed CG iterations per step")
     p.add_argument("--batch", type=int, default=0)
@@ -57,15 +59,22 @@ def model_bytes(solver, N, F, P):
     return 136 * N + 16 * F + 28 * P
 
 
-def pass_model_bytes(solver, N, F):
-    """Dominant kernel per launch, §8(d): classical pass A = 56N + 16F; pipelined pass U = 112N."""
-    return 56 * N + 16 * F if solver == "pcg" else 112 * N
+def pass_model_bytes(solver, N, F, fused=False):
+    """Dominant kernel per launch, §8(d): classical pass A = 56N + 16F; pipelined pass U = 112N
+    (single rank: S and U fused into one pass = the whole iteration, 136N + 16F)."""
+    if solver == "pcg":
+        return 56 * N + 16 * F
+    return 136 * N + 16 * F if fused else 112 * N
 
 
 def pass_format_bytes(solver, info, N):
     """Bytes the dominant kernel must move in the layout it actually streams."""
     if solver == "pipecg":
-        return 112 * N
+        if not info.get("pipeFused"):
+            return 112 * N
+        if info["layout_name"] == "DIA_SYM":  # w, rD, z, s, r, p, x, U_k in; z, s, p, x, r, w out
+            return (13 + info["nDiagonals"]) * 8 * N
+        return 104 * N + 12 * info["storedEntries"] + 12 * ((N + 31) // 32)
     if info["layout_name"] == "DIA_SYM":
         return 56 * N + 8 * info["nDiagonals"] * N  # r, rD, p_old, x in; p, q, x out; U_k once
     return 56 * N + 12 * info["storedEntries"] + 12 * ((N + 31) // 32)
@@ -255,7 +264,6 @@ def main():
     A.set_stream(stream.cuda_stream)
     b = torch.from_numpy(sys_.b).cuda()
     x = torch.zeros_like(b)
-    solve = A.pcg_solve if args.solver == "pcg" else A.pipecg_solve
     kw = dict(tol=0.0, maxIter=args.iters, batch=args.batch)
 
     def barrier():
@@ -263,59 +271,79 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(3, args.warmup)):
-        x.zero_()
-        solve(b, x, **kw)
-    barrier()
-
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    kernels = 0
-    pass_ms, pass_n = 0.0, 0
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        x.zero_()
-        st, it, res = solve(b, x, profile=not args.no_profile, **kw)
-        s = A.stats()
-        kernels += s["kernels"]
-        pass_ms += s["passMs"][0 if args.solver == "pcg" else 1]
-        pass_n += s["passLaunches"][0 if args.solver == "pcg" else 1]
-    e1.record(stream)
-    barrier()
-    elapsed = e0.elapsed_time(e1) / 1e3
-    clk = clocks.stop()
-    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed = float(t.item())
-    value = args.steps * args.iters / elapsed
-
     # global byte model
     tot = torch.tensor([N, F, P], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(tot)
     Ng, Fg, Pg = (float(v) for v in tot.tolist())
-    bytes_iter = model_bytes(args.solver, Ng, Fg, Pg)
     peak, peak_src = hbm_peak()
 
-    # roofline of the dominant kernel (this rank), measured live with CUDA events in the graph
-    roof = None
-    if pass_n:
-        t_launch = pass_ms / pass_n / 1e3
-        mb = pass_model_bytes(args.solver, N, F)
-        fb = pass_format_bytes(args.solver, info, N)
-        traffic = ncu_traffic(args.solver, n, world)
-        roof = {"kernel": "k_cg_passA" if args.solver == "pcg" else "k_pipe_U",
-                "bound": "hbm", "achieved": mb / t_launch / 1e9, "peak": peak, "unit": "GB/s",
-                "frac": mb / t_launch / 1e9 / peak, "traffic": traffic,
-                "model_bytes_per_launch": mb, "launch_us": t_launch * 1e6,
-                "format_bytes_per_launch": fb, "format_achieved": fb / t_launch / 1e9,
-                "format_frac": fb / t_launch / 1e9 / peak, "peak_source": peak_src,
-                "share_of_step": pass_ms / 1e3 / elapsed}
+    def timed(solver, sample_clocks):
+        """W warm-up solves, then K timed solves bracketed by barrier + synchronize; device time
+        by CUDA events on the caller's stream, max over ranks."""
+        fn = A.pcg_solve if solver == "pcg" else A.pipecg_solve
+        for _ in range(max(3, args.warmup)):
+            x.zero_()
+            fn(b, x, **kw)
+        barrier()
+        clocks = ClockSampler(local) if sample_clocks else None
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        kernels, pass_ms, pass_n = 0, 0.0, 0
+        slot = 0 if solver == "pcg" else 1
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            x.zero_()
+            st, it, res = fn(b, x, profile=not args.no_profile, **kw)
+            s = A.stats()
+            kernels += s["kernels"]
+            pass_ms += s["passMs"][slot]
+            pass_n += s["passLaunches"][slot]
+        e1.record(stream)
+        barrier()
+        elapsed = e0.elapsed_time(e1) / 1e3
+        clk = clocks.stop() if clocks else None
+        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        value = args.steps * args.iters / elapsed
+        # roofline of the dominant kernel (this rank), timed live with CUDA event nodes
+        roof = None
+        if pass_n:
+            t_launch = pass_ms / pass_n / 1e3
+            fused = bool(info.get("pipeFused")) and solver == "pipecg"
+            mb = pass_model_bytes(solver, N, F, fused)
+            fb = pass_format_bytes(solver, info, N)
+            roof = {"kernel": "k_cg_passA" if solver == "pcg" else ("k_pipe_SU" if fused else "k_pipe_U"),
+                    "bound": "hbm", "achieved": mb / t_launch / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": mb / t_launch / 1e9 / peak, "traffic": ncu_traffic(solver, n, world),
+                    "model_bytes_per_launch": mb, "launch_us": t_launch * 1e6,
+                    "format_bytes_per_launch": fb, "format_achieved": fb / t_launch / 1e9,
+                    "format_frac": fb / t_launch / 1e9 / peak, "peak_source": peak_src,
+                    "share_of_step": pass_ms / 1e3 / elapsed}
+        bytes_iter = model_bytes(solver, Ng, Fg, Pg)
+        return dict(value=value, elapsed=elapsed, kernels=kernels, roof=roof, clk=clk,
+                    status=int(st), iters=it, bytes_iter=bytes_iter,
+                    eff=value * bytes_iter / 1e9)
+
+    main_r = timed(args.solver, True)
+    value, elapsed, kernels = main_r["value"], main_r["elapsed"], main_r["kernels"]
+    roof, clk, bytes_iter = main_r["roof"], main_r["clk"], main_r["bytes_iter"]
+    st, it = main_r["status"], main_r["iters"]
+    secondary = None
+    if not args.no_secondary:
+        other = "pcg" if args.solver == "pipecg" else "pipecg"
+        r2 = timed(other, False)
+        secondary = {"solver": other, "value": r2["value"], "unit": UNIT,
+                     "ms_per_step": 1e3 * r2["elapsed"] / args.steps,
+                     "effective_gbps": r2["eff"], "bytes_per_iter_model": r2["bytes_iter"],
+                     "effective_frac_of_hbm": r2["eff"] / (peak * world), "roofline": r2["roof"]}
+    solve = A.pcg_solve if args.solver == "pcg" else A.pipecg_solve
 
     # end to end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -363,6 +391,7 @@ def main():
                "effective_frac_of_hbm": value * bytes_iter / 1e9 / (peak * world),
                "bytes_per_iter_model": bytes_iter,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels,
+               "secondary": secondary,
                "clocks": clk, "last_status": int(st), "iterations_per_step": it}
         print(json.dumps(out), flush=True)
     A.close()

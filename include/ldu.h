@@ -180,6 +180,8 @@ typedef struct {
   long long matrixBytes;   /* device bytes of the matrix layout (incl. diag and 1/diag)         */
   int nCells, nFaces, nInterfaceFaces, nRanks, rank;
   int gridBlocks, blockThreads;
+  int variant;           /* SpMV-pass kernel variant in use (env LDU_VARIANT)          */
+  int pipeFused;         /* 1: single-rank pipelined CG runs S and U as one fused pass            */
 } ldu_info;
 
 ldu_status ldu_get_info(ldu_handle h, ldu_info *out);

@@ -75,7 +75,8 @@ class Info(ctypes.Structure):
                 ("matrixBytes", ctypes.c_longlong), ("nCells", ctypes.c_int),
                 ("nFaces", ctypes.c_int), ("nInterfaceFaces", ctypes.c_int),
                 ("nRanks", ctypes.c_int), ("rank", ctypes.c_int), ("gridBlocks", ctypes.c_int),
-                ("blockThreads", ctypes.c_int)]
+                ("blockThreads", ctypes.c_int), ("variant", ctypes.c_int),
+                ("pipeFused", ctypes.c_int)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -250,6 +250,8 @@ ldu_status ldu_get_info(ldu_handle h, ldu_info* out) {
     out->rank = h->rank;
     out->gridBlocks = h->grid;
     out->blockThreads = h->block;
+    out->variant = h->variant;
+    out->pipeFused = (h->fusePipe && !(h->comm && h->comm->nRanks > 1)) ? 1 : 0;
     return LDU_OK;
   });
 }

@@ -130,7 +130,7 @@ struct ldu_handle_s {
   double* rD = nullptr;
   // work vectors (lazily allocated)
   double *x = nullptr, *r = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr;
-  double *w = nullptr, *nv = nullptr, *z = nullptr, *s = nullptr;
+  double *w = nullptr, *w2 = nullptr, *nv = nullptr, *z = nullptr, *s = nullptr;
   double *bbuf = nullptr, *ybuf = nullptr;
   // reductions
   double* partials = nullptr;  // [kMaxVals][maxParts]
@@ -149,6 +149,7 @@ struct ldu_handle_s {
   bool tmaOk = false, tmaStrict = false;  // TMA plane march (variant 4)
   int tT = 0, tTiles = 0, tChunk = 0, tGrid = 0, tL = 1;
   int chunkK = 2048;                  // variant 5: rows per chunk
+  bool fusePipe = true;               // single rank: pipelined S+U fused (LDU_PIPE_FUSE)
   // history
   double* hist = nullptr;
   int histCap = 0;

@@ -342,6 +342,45 @@ __global__ void __launch_bounds__(kBlock) k_pipe_U(int n, const double* __restri
   finish_reduction<3>(v, rd, st);
 }
 
+// pipelined, single rank: passes S_i and U_i fused.  With one rank there is no global reduction
+// to hide behind the SpMV, so n_i = A (rD.w_i) is consumed row by row and never stored (saves the
+// 16N bytes of writing and re-reading n).  w is ping-pong buffered: neighbours gather w_i while
+// the pass writes w_{i+1}.
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_pipe_SU(Fmt A, const double* __restrict__ rD,
+                                                    double* w0, double* w1,
+                                                    double* __restrict__ z, double* __restrict__ s,
+                                                    double* __restrict__ p, double* __restrict__ x,
+                                                    double* __restrict__ r, State* st, Red rd) {
+  if (st->done) return;
+  const double a = st->pa, b = st->pb;
+  const bool l2 = st->norm == LDU_NORM_L2;
+  const double* __restrict__ w = (st->k & 1) ? w1 : w0;
+  double* __restrict__ wn = (st->k & 1) ? w0 : w1;
+  double v[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(c, A.n) {
+    const double wc0 = __ldg(w + c);
+    const double nc = row_apply(A, c, wc0, [&](int j) { return __ldg(rD + j) * __ldg(w + j); });
+    const double rdc = __ldg(rD + c), rc0 = r[c];
+    const double zc = fma(b, z[c], nc);
+    const double sc = fma(b, s[c], wc0);
+    const double pc = fma(b, p[c], rdc * rc0);
+    z[c] = zc;
+    s[c] = sc;
+    p[c] = pc;
+    x[c] = fma(a, pc, x[c]);
+    const double rc = fma(-a, sc, rc0);
+    const double wc = fma(-a, zc, wc0);
+    r[c] = rc;
+    wn[c] = wc;
+    const double u = rdc * rc;
+    v[0] = fma(rc, u, v[0]);
+    v[1] = fma(wc, u, v[1]);
+    v[2] += l2 ? rc * rc : fabs(rc);
+  }
+  finish_reduction<3>(v, rd, st);
+}
+
 // multi-rank control: sum the allgathered per-rank sums in rank order, then run the step.
 __global__ void k_ctl(int ctl, State* st, const double* __restrict__ gsums, int nRanks, int nv) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -674,6 +713,7 @@ void ensure_work(ldu_handle h, bool pipelined) {
   } else {
     ensure_vec(h->w, n);
     ensure_vec(h->nv, n);
+    if (!multi(h) && h->fusePipe) ensure_vec(h->w2, n);
     ensure_vec(h->z, n);
     ensure_vec(h->s, n);
     ensure_vec(h->p0, n);
@@ -730,6 +770,20 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
 long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profile) {
   long long kernels = 0;
   const bool mr = multi(h);
+  if (!mr && h->fusePipe) {  // one fused pass per iteration (profile: pass slot 1)
+    for (int it = 0; it < batch; ++it) {
+      prof_mark(h, profile, 4 * it + 0, s);
+      prof_mark(h, profile, 4 * it + 1, s);
+      prof_mark(h, profile, 4 * it + 2, s);
+      with_format(h, [&](auto A) {
+        k_pipe_SU<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x,
+                                               h->r, h->st, red_of(h, CTL_PIPE_NEXT, true, h->gridA));
+      });
+      prof_mark(h, profile, 4 * it + 3, s);
+      ++kernels;
+    }
+    return kernels;
+  }
   const bool haveIf = h->nIfFaces > 0;
   ldu_comm cm = h->comm;
   for (int it = 0; it < batch; ++it) {
@@ -1041,7 +1095,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
 }
 
 void release_work(ldu_handle h) {
-  for (double** p : {&h->x, &h->r, &h->p0, &h->p1, &h->q, &h->w, &h->nv, &h->z, &h->s,
+  for (double** p : {&h->x, &h->r, &h->p0, &h->p1, &h->q, &h->w, &h->w2, &h->nv, &h->z, &h->s,
                      &h->bbuf, &h->ybuf, &h->hist}) {
     dfree(*p);
     *p = nullptr;
@@ -1064,6 +1118,8 @@ void configure(ldu_handle h) {
   if (const char* v = std::getenv("LDU_VARIANT")) h->variant = std::atoi(v);
   if (h->variant < 0 || h->variant > 5) h->variant = 0;
   h->chunkK = 2048;
+  h->fusePipe = true;
+  if (const char* v = std::getenv("LDU_PIPE_FUSE")) h->fusePipe = std::atoi(v) != 0;
   if (const char* v = std::getenv("LDU_CHUNK")) h->chunkK = std::max(256, std::atoi(v) / 256 * 256);
   const long long need = ((long long)h->n + kBlock - 1) / kBlock;
   auto grid_of = [&](const void* fn) {

@@ -76,3 +76,30 @@ def test_solve_variants(ldu, mesh, variant, solver):
     _, oxf, _, _ = ofn(sys, sys.b, tol=0.0, maxIter=17)
     assert st2 == ldu.NOT_CONVERGED and it2 == 17
     assert np.linalg.norm(xf - oxf) <= 1e-11 * np.linalg.norm(oxf)
+
+
+@pytest.mark.parametrize("fuse", [0, 1])
+@pytest.mark.parametrize("mesh", sorted(MESHES))
+def test_pipelined_fused_and_split(ldu, mesh, fuse):
+    """Single rank: pipelined CG with S and U fused (default) and split (LDU_PIPE_FUSE=0)."""
+    sys = MESHES[mesh]()
+    ost, ox, oit, ores = oracle.pipecg(sys, sys.b, tol=1e-10, maxIter=5000)
+    old = os.environ.get("LDU_PIPE_FUSE")
+    os.environ["LDU_PIPE_FUSE"] = str(fuse)
+    try:
+        A = ldu.LduMatrix.from_system(sys)
+    finally:
+        if old is None:
+            del os.environ["LDU_PIPE_FUSE"]
+        else:
+            os.environ["LDU_PIPE_FUSE"] = old
+    with A:
+        assert A.info()["pipeFused"] == fuse
+        x = np.zeros(sys.nCells)
+        st, it, res = A.pipecg_solve(sys.b, x, tol=1e-10, maxIter=5000)
+        xf = np.zeros(sys.nCells)
+        A.pipecg_solve(sys.b, xf, tol=0.0, maxIter=23)
+    assert st == ldu.OK and abs(it - oit) <= max(1, round(0.02 * oit))
+    assert np.linalg.norm(x - ox) <= 1e-8 * np.linalg.norm(ox)
+    _, oxf, _, _ = oracle.pipecg(sys, sys.b, tol=0.0, maxIter=23)
+    assert np.linalg.norm(xf - oxf) <= 1e-11 * np.linalg.norm(oxf)
