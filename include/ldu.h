@@ -91,6 +91,9 @@ ldu_status ldu_comm_destroy(ldu_comm comm);
  *   lower [nFaces] or NULL, upper [nFaces]
  *   interfaces: NULL for a single-rank matrix.
  * All arrays may be host or device pointers and are copied: the caller may free them on return.
+ * With a multi-rank comm, ldu_setup is COLLECTIVE: it maps every rank's communication mailbox
+ * (CUDA IPC over NVLink) and pairs the interfaces with the neighbours' (an interface without a
+ * matching one of equal face count on its neighbour is LDU_ERR_INVALID_ARG).
  * The one-time conversion runs on the device; it chooses a row-gathered, cell-ordered layout
  * (DESIGN.md "Data layout"): symmetric banded matrices get a symmetric diagonal (DIA) layout
  * storing each face coefficient once; others a SELL-32 layout.  Both are deterministic: SpMV

@@ -34,6 +34,7 @@ void destroy_handle(ldu_handle h) {
   cudaSetDevice(h->device);
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   ldu::release_work(h);
+  ldu::p2p_release(h);
   for (void* p : {(void*)h->U, (void*)h->slicePtr, (void*)h->npairs, (void*)h->col,
                   (void*)h->val, (void*)h->diag, (void*)h->rD, (void*)h->partials,
                   (void*)h->ticket, (void*)h->sums, (void*)h->gsums, (void*)h->st,
@@ -251,7 +252,7 @@ ldu_status ldu_get_info(ldu_handle h, ldu_info* out) {
     out->gridBlocks = h->grid;
     out->blockThreads = h->block;
     out->variant = h->variant;
-    out->pipeFused = (h->fusePipe && !(h->comm && h->comm->nRanks > 1)) ? 1 : 0;
+    out->pipeFused = (h->fusePipe && (!(h->comm && h->comm->nRanks > 1) || h->p2pOn)) ? 1 : 0;
     return LDU_OK;
   });
 }

@@ -94,6 +94,8 @@ struct State {
 // ---------------------------------------------------------------------------------------------
 // handle / comm
 // ---------------------------------------------------------------------------------------------
+struct P2PDesc;  // ldu_p2p.cuh
+
 struct DevInterface {
   int neighbRank;
   int nFaces;
@@ -162,6 +164,7 @@ struct ldu_handle_s {
   };
   Graph graphs[2][2];       // [pipelined][profile]
   std::vector<cudaEvent_t> prof_ev;  // profile mode: 4 events per iteration of a batch
+  std::vector<cudaEvent_t> trace;    // LDU_TRACE debug events
   // interfaces
   ldu_comm comm = nullptr;
   int nRanks = 1, rank = 0;
@@ -180,9 +183,18 @@ struct ldu_handle_s {
   cudaEvent_t ev_fork = nullptr, ev_red = nullptr, ev_halo = nullptr, ev_pack = nullptr;
   ldu_solve_stats stats = {};
   long long matrixBytes = 0;
+  // NVLink peer-memory communication (multi-rank; ldu_p2p.cuh)
+  bool p2pOn = false;
+  char* mailbox = nullptr;               // this rank's mailbox (peers write into it)
+  std::vector<char*> peerMailbox;        // IPC-mapped mailboxes of the other ranks
+  ldu::P2PDesc* p2pDesc = nullptr;       // device descriptor
+  int* ifFaceIf = nullptr;               // [nIfFaces] interface index of each packed face
 };
 
 namespace ldu {
+struct P2PDesc;
+void p2p_setup(ldu_handle h);
+void p2p_release(ldu_handle h);
 // setup (ldu_setup.cu)
 void build_layout(ldu_handle h, const int* l, const int* u, const double* diag,
                   const double* lower, const double* upper, const ldu_interfaces* ifs);

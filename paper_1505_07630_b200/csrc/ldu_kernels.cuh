@@ -9,6 +9,7 @@
 #pragma once
 
 #include "ldu_impl.cuh"
+#include "ldu_p2p.cuh"
 
 namespace ldu {
 
@@ -243,6 +244,7 @@ struct Red {  // reduction plumbing of one pass
   int slot_base;   // first partial slot of this kernel
   int total;       // slots summed by the last block
   int store_only;  // 1: store partials only (a later kernel finishes the reduction)
+  P2PDesc* p2p;    // multi-rank over peer memory: publish the local sums to every rank
 };
 
 template <int NV>
@@ -259,6 +261,7 @@ __device__ __forceinline__ void finish_reduction(double (&v)[NV], const Red& rd,
                                 gridDim.x)) {
     sum_partials<NV>(rd.partials, rd.ld, rd.total, rd.sums, rd.ticket);
     if (threadIdx.x == 0 && rd.ctl != CTL_NONE) run_ctl(rd.ctl, st, rd.sums);
+    if (threadIdx.x == 0 && rd.p2p) p2p_publish_sums<NV>(rd.p2p, rd.sums);
   }
 }
 

@@ -1,0 +1,109 @@
+// ldu_p2p.cuh -- NVLink peer-memory communication fused into the CG kernels (multi-rank).
+//
+// Every rank owns one "mailbox" allocation that its peers write into over NVLink (CUDA IPC
+// mappings, one process per GPU):
+//   redFlag[2][kP2PMaxRanks]  u64   reduction flags, slot [parity][source rank]
+//   haloFlag[2][kP2PMaxIf]    u64   halo flags, slot [parity][receiving interface]
+//   red[2][kP2PMaxRanks][4]   f64   the fused partial sums, slot [parity][source rank]
+//   recv[2][nIfFaces]         f64   halo values, double-buffered by exchange parity
+// Messages carry a sequence number (per handle, identical on every rank because all ranks run
+// the same sequence of collective steps).  Producers store data, __threadfence_system(), then
+// store the flag = seq; consumers spin (bounded, then trap) until flag >= seq and read with
+// L1-bypassing loads.  Parity double-buffering is sufficient: a peer can run at most one
+// exchange ahead because it needs this rank's reduction contribution to proceed.
+#pragma once
+
+#include <cstdint>
+
+#include "ldu_impl.cuh"
+
+namespace ldu {
+
+constexpr int kP2PMaxRanks = 64;
+constexpr int kP2PMaxIf = 16;
+
+struct MailboxLayout {
+  static constexpr size_t redFlag = 0;
+  static constexpr size_t haloFlag = redFlag + sizeof(uint64_t) * 2 * kP2PMaxRanks;
+  static constexpr size_t red = haloFlag + sizeof(uint64_t) * 2 * kP2PMaxIf;
+  static constexpr size_t recv = red + sizeof(double) * 2 * kP2PMaxRanks * 4;
+  static size_t bytes(int nIfFaces) { return recv + sizeof(double) * 2 * (size_t)nIfFaces; }
+};
+
+// Device-resident descriptor (one per handle).
+struct P2PDesc {
+  int rank, nRanks, nIf;
+  unsigned long long seqRed, seqHalo;   // last completed sequence numbers (device state)
+  char* base[kP2PMaxRanks];             // mailbox of every rank (own = local pointer)
+  int ifNeighbor[kP2PMaxIf];            // peer rank of my interface k
+  int ifLocalOff[kP2PMaxIf];            // my packed face offset of interface k
+  int ifNFaces[kP2PMaxIf];
+  int ifRemoteOff[kP2PMaxIf];           // offset in the peer's recv of its interface back to me
+  int ifRemoteIdx[kP2PMaxIf];           // the peer's interface index (its halo flag slot)
+  int ifRemoteTotal[kP2PMaxIf];         // the peer's packed interface face count (recv stride)
+};
+
+__device__ __forceinline__ uint64_t* mb_redflag(char* b, int par, int src) {
+  return reinterpret_cast<uint64_t*>(b + MailboxLayout::redFlag) + par * kP2PMaxRanks + src;
+}
+__device__ __forceinline__ uint64_t* mb_haloflag(char* b, int par, int k) {
+  return reinterpret_cast<uint64_t*>(b + MailboxLayout::haloFlag) + par * kP2PMaxIf + k;
+}
+__device__ __forceinline__ double* mb_red(char* b, int par, int src) {
+  return reinterpret_cast<double*>(b + MailboxLayout::red) + (par * kP2PMaxRanks + src) * 4;
+}
+__device__ __forceinline__ double* mb_recv(char* b, int par, int nIfFaces) {
+  return reinterpret_cast<double*>(b + MailboxLayout::recv) + (size_t)par * nIfFaces;
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Bounded spin (~4 s at 2 GHz): a lost peer turns into a kernel error, not a hung GPU.
+__device__ __forceinline__ void spin_until_geq(const uint64_t* p, uint64_t seq) {
+  const long long t0 = clock64();
+  while (ld_acquire_sys(p) < seq) {
+    if (clock64() - t0 > 8000000000LL) __trap();
+    __nanosleep(64);
+  }
+}
+
+// Last block of a reducing pass: publish the local sums to every rank's mailbox (incl. self).
+template <int NV>
+__device__ __forceinline__ void p2p_publish_sums(P2PDesc* d, const double* sums) {
+  const uint64_t seq = d->seqRed + 1;
+  const int par = (int)(seq & 1);
+  for (int r = 0; r < d->nRanks; ++r) {
+    double* dst = mb_red(d->base[r], par, d->rank);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) dst[k] = sums[k];
+  }
+  // the release stores order this thread's data stores before the flags (no full fence needed)
+  for (int r = 0; r < d->nRanks; ++r) st_release_sys(mb_redflag(d->base[r], par, d->rank), seq);
+}
+
+// Control kernel side: wait for every rank's sums of the next sequence number, sum them in
+// rank order into s[], advance the sequence.
+template <int NV>
+__device__ __forceinline__ void p2p_gather_sums(P2PDesc* d, double* s) {
+  const uint64_t seq = d->seqRed + 1;
+  const int par = (int)(seq & 1);
+  char* me = d->base[d->rank];
+  for (int k = 0; k < NV; ++k) s[k] = 0.0;
+  for (int r = 0; r < d->nRanks; ++r) {
+    spin_until_geq(mb_redflag(me, par, r), seq);
+    const double* src = mb_red(me, par, r);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) s[k] += __ldcv(src + k);
+  }
+  d->seqRed = seq;
+}
+
+}  // namespace ldu

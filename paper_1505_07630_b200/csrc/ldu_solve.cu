@@ -14,6 +14,7 @@
 // Scalars never leave the device; iterations run as CUDA-graph batches whose kernels exit at
 // entry once the device `done` flag is set; the host reads the state once per batch.
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include <vector>
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(kBlock) k_iface_cg(int nIfCells, const int* __
   finish_reduction<1>(v, rd, st);
 }
 
-enum Pack : int { PACK_PLAIN = 0, PACK_SCALED = 1, PACK_CG_P = 2 };
+enum Pack : int { PACK_PLAIN = 0, PACK_SCALED = 1, PACK_CG_P = 2, PACK_SCALED_W = 3 };
 
 // Halo send buffer: the SpMV operand at the interface cells.
 __global__ void k_pack(int nIfFaces, const int* __restrict__ fc, int mode,
@@ -381,6 +382,137 @@ __global__ void __launch_bounds__(kBlock) k_pipe_SU(Fmt A, const double* __restr
   finish_reduction<3>(v, rd, st);
 }
 
+// ---- NVLink peer-memory halo and reductions (ldu_p2p.cuh) ----------------------------------
+
+// Halo send fused with the pack: the operand at every interface face is stored straight into the
+// neighbour's mailbox over NVLink; the last block raises the neighbours' flags.
+__global__ void __launch_bounds__(kBlock) k_pack_p2p(int nIfFaces, const int* __restrict__ fc,
+                                                     const int* __restrict__ faceIf, int mode,
+                                                     const double* a,
+                                                     const double* __restrict__ rD,
+                                                     const double* p0, const double* p1,
+                                                     const State* st, P2PDesc* d,
+                                                     unsigned* ticket) {
+  if (st->done) return;
+  double beta = 0.0;
+  const double* pold = nullptr;
+  if (mode == PACK_CG_P) {
+    beta = st->beta;
+    pold = (st->k & 1) ? p0 : p1;
+  }
+  const unsigned long long seq = d->seqHalo + 1;
+  const int par = (int)(seq & 1);
+  if (mode == PACK_SCALED_W) a = (st->k & 1) ? p1 : p0;  // w_i of the fused pipelined pass
+  GRID_STRIDE(i, nIfFaces) {
+    const int c = fc[i];
+    double v = a[c];
+    if (mode == PACK_SCALED || mode == PACK_SCALED_W) v = rD[c] * v;
+    else if (mode == PACK_CG_P) v = fma(beta, pold[c], rD[c] * v);
+    const int k = faceIf[i];
+    double* dst = mb_recv(d->base[d->ifNeighbor[k]], par, d->ifRemoteTotal[k]);
+    dst[d->ifRemoteOff[k] + (i - d->ifLocalOff[k])] = v;
+  }
+  // one cumulative system-scope fence per block (after the barrier) orders the whole block's
+  // remote stores before its ticket; the last block then releases the flags
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int k = 0; k < d->nIf; ++k)
+      st_release_sys(mb_haloflag(d->base[d->ifNeighbor[k]], par, d->ifRemoteIdx[k]), seq);
+    *ticket = 0u;
+  }
+}
+
+// Wait for this exchange's halo (flags of all my interfaces), then read my mailbox.
+__device__ __forceinline__ const double* p2p_wait_halo(P2PDesc* d, int nIfFaces) {
+  const unsigned long long seq = d->seqHalo + 1;
+  const int par = (int)(seq & 1);
+  char* me = d->base[d->rank];
+  if ((int)threadIdx.x < d->nIf) spin_until_geq(mb_haloflag(me, par, threadIdx.x), seq);
+  __syncthreads();
+  return mb_recv(me, par, nIfFaces);
+}
+
+__global__ void k_iface_apply_p2p(int nIfCells, const int* __restrict__ cell,
+                                  const int* __restrict__ ptr, const int* __restrict__ fidx,
+                                  const double* __restrict__ coeff, double* __restrict__ y,
+                                  const State* st, P2PDesc* d, int nIfFaces) {
+  if (st->done) return;
+  const double* recv = p2p_wait_halo(d, nIfFaces);
+  GRID_STRIDE(i, nIfCells) {
+    double corr = 0.0;
+    for (int t = ptr[i]; t < ptr[i + 1]; ++t) corr = fma(coeff[fidx[t]], __ldcv(recv + fidx[t]), corr);
+    y[cell[i]] -= corr;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_iface_cg_p2p(int nIfCells, const int* __restrict__ cell,
+                                                         const int* __restrict__ ptr,
+                                                         const int* __restrict__ fidx,
+                                                         const double* __restrict__ coeff,
+                                                         double* __restrict__ q, const double* p0,
+                                                         const double* p1, State* st, Red rd,
+                                                         P2PDesc* d, int nIfFaces) {
+  if (st->done) return;
+  const double* recv = p2p_wait_halo(d, nIfFaces);
+  const double* __restrict__ pnew = (st->k & 1) ? p1 : p0;
+  double v[1] = {0.0};
+  GRID_STRIDE(i, nIfCells) {
+    double corr = 0.0;
+    for (int t = ptr[i]; t < ptr[i + 1]; ++t) corr = fma(coeff[fidx[t]], __ldcv(recv + fidx[t]), corr);
+    const int c = cell[i];
+    q[c] -= corr;
+    v[0] -= pnew[c] * corr;
+  }
+  finish_reduction<1>(v, rd, st);
+}
+
+// Multi-rank fused pipelined pass, fix-up of the interface rows once the halo has arrived:
+// k_pipe_SU used the internal part of n at every row; n is linear in the interface term
+// dn = -sum coeff * recv, so z += dn, w_{i+1} -= alpha dn and the delta partial gains
+// -alpha dn (rD r_{i+1}) -- exact algebra, rows touched only here.
+__global__ void __launch_bounds__(kBlock) k_pipe_fixup_p2p(int nIfCells, const int* __restrict__ cell,
+                                                           const int* __restrict__ ptr,
+                                                           const int* __restrict__ fidx,
+                                                           const double* __restrict__ coeff,
+                                                           const double* __restrict__ rD,
+                                                           const double* __restrict__ r,
+                                                           double* __restrict__ z, double* w0,
+                                                           double* w1, State* st, Red rd,
+                                                           P2PDesc* d, int nIfFaces) {
+  if (st->done) return;
+  const double* recv = p2p_wait_halo(d, nIfFaces);
+  const double a = st->pa;
+  double* __restrict__ wn = (st->k & 1) ? w0 : w1;
+  double v[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(i, nIfCells) {
+    double corr = 0.0;
+    for (int t = ptr[i]; t < ptr[i + 1]; ++t) corr = fma(coeff[fidx[t]], __ldcv(recv + fidx[t]), corr);
+    const int c = cell[i];
+    const double dn = -corr;
+    z[c] += dn;
+    wn[c] = fma(-a, dn, wn[c]);
+    v[1] = fma(-a * dn, rD[c] * r[c], v[1]);
+  }
+  finish_reduction<3>(v, rd, st);
+}
+
+// Control step after a peer-memory reduction: wait for every rank's sums, rank-ordered sum.
+__global__ void k_ctl_p2p(int ctl, State* st, P2PDesc* d, int advanceHalo) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (st->done) return;
+  double s[kMaxVals];
+  p2p_gather_sums<kMaxVals>(d, s);
+  if (advanceHalo) d->seqHalo += 1;
+  run_ctl(ctl, st, s);
+}
+
 // multi-rank control: sum the allgathered per-rank sums in rank order, then run the step.
 __global__ void k_ctl(int ctl, State* st, const double* __restrict__ gsums, int nRanks, int nv) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -641,7 +773,33 @@ Red red_of(ldu_handle h, int ctl, bool single, int grid = 0) {
   r.slot_base = 0;
   r.total = grid ? grid : h->grid;
   r.store_only = 0;
+  r.p2p = nullptr;
   return r;
+}
+
+// loop-pass reduction: over peer memory when enabled (multi-rank), else as red_of
+Red red_loop(ldu_handle h, int ctl, bool single, int grid = 0) {
+  Red r = red_of(h, ctl, single, grid);
+  if (!single && h->p2pOn) r.p2p = h->p2pDesc;
+  return r;
+}
+
+// fork the NVLink halo send onto the halo stream (it overlaps the next bulk pass) / join it
+void p2p_pack(ldu_handle h, int mode, const double* a, cudaStream_t s);
+void p2p_pack_async(ldu_handle h, int mode, const double* a, cudaStream_t s) {
+  CUDA_CHECK(cudaEventRecord(h->ev_pack, s));
+  CUDA_CHECK(cudaStreamWaitEvent(h->halo_stream, h->ev_pack, 0));
+  p2p_pack(h, mode, a, h->halo_stream);
+  CUDA_CHECK(cudaEventRecord(h->ev_halo, h->halo_stream));
+}
+void p2p_join(ldu_handle h, cudaStream_t s) { CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_halo, 0)); }
+
+void p2p_pack(ldu_handle h, int mode, const double* a, cudaStream_t s) {
+  const double* q0 = mode == PACK_SCALED_W ? h->w : h->p0;
+  const double* q1 = mode == PACK_SCALED_W ? h->w2 : h->p1;
+  k_pack_p2p<<<small_grid(h->nIfFaces), kBlock, 0, s>>>(
+      h->nIfFaces, h->ifFaceCells, h->ifFaceIf, mode, a, h->rD, q0, q1, h->st, h->p2pDesc,
+      h->ticket + 1);
 }
 
 bool multi(ldu_handle h) { return h->comm && h->comm->nRanks > 1; }
@@ -713,7 +871,7 @@ void ensure_work(ldu_handle h, bool pipelined) {
   } else {
     ensure_vec(h->w, n);
     ensure_vec(h->nv, n);
-    if (!multi(h) && h->fusePipe) ensure_vec(h->w2, n);
+    if (h->fusePipe && (!multi(h) || h->p2pOn)) ensure_vec(h->w2, n);
     ensure_vec(h->z, n);
     ensure_vec(h->s, n);
     ensure_vec(h->p0, n);
@@ -721,6 +879,13 @@ void ensure_work(ldu_handle h, bool pipelined) {
 }
 
 // One batch of `batch` iterations, enqueued on s (captured into a graph by the caller).
+// LDU_TRACE=1 (debug): 5 external event nodes per iteration of the fused multi-rank pipelined
+// loop; the per-segment device times are printed to stderr after each solve.
+void trace_mark(ldu_handle h, int it, int k, cudaStream_t s) {
+  if (!h->trace.empty())
+    CUDA_CHECK(cudaEventRecordWithFlags(h->trace[5 * it + k], s, cudaEventRecordExternal));
+}
+
 void prof_mark(ldu_handle h, bool profile, int idx, cudaStream_t s) {
   // external event nodes: recorded by the graph on every launch (plain records inside a capture
   // only express dependencies)
@@ -731,6 +896,38 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
   long long kernels = 0;
   const bool mr = multi(h);
   const bool haveIf = h->nIfFaces > 0;
+  if (mr && h->p2pOn) {  // halo and both reductions over NVLink peer memory, no NCCL kernels
+    for (int it = 0; it < batch; ++it) {
+      if (haveIf) {
+        p2p_pack_async(h, PACK_CG_P, h->r, s);
+        ++kernels;
+      }
+      Red ra = red_loop(h, CTL_CG_A, false, h->gridA);
+      if (haveIf) ra.store_only = 1;
+      prof_mark(h, profile, 4 * it + 0, s);
+      launch_passA(h, ra, s);
+      prof_mark(h, profile, 4 * it + 1, s);
+      ++kernels;
+      if (haveIf) {
+        p2p_join(h, s);
+        Red ri = red_loop(h, CTL_CG_A, false);
+        const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->gridA);
+        ri.slot_base = h->gridA;
+        ri.total = h->gridA + ig;
+        k_iface_cg_p2p<<<ig, kBlock, 0, s>>>(h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx,
+                                             h->ifCoeffs, h->q, h->p0, h->p1, h->st, ri,
+                                             h->p2pDesc, h->nIfFaces);
+        ++kernels;
+      }
+      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_CG_A, h->st, h->p2pDesc, haveIf ? 1 : 0);
+      prof_mark(h, profile, 4 * it + 2, s);
+      k_cg_passB<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->q, h->r, h->st, red_loop(h, CTL_CG_B, false));
+      prof_mark(h, profile, 4 * it + 3, s);
+      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_CG_B, h->st, h->p2pDesc, 0);
+      kernels += 3;
+    }
+    return kernels;
+  }
   for (int it = 0; it < batch; ++it) {
     // pass A
     if (haveIf) {
@@ -770,6 +967,72 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
 long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profile) {
   long long kernels = 0;
   const bool mr = multi(h);
+  if (mr && h->p2pOn && h->fusePipe) {  // fused S+U pass per iteration over peer memory
+    const bool haveIf = h->nIfFaces > 0;
+    for (int it = 0; it < batch; ++it) {
+      trace_mark(h, it, 0, s);
+      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_PIPE_NEXT, h->st, h->p2pDesc, haveIf ? 1 : 0);
+      trace_mark(h, it, 1, s);
+      ++kernels;
+      if (haveIf) {  // on the halo stream: the NVLink halo send overlaps the bulk pass below
+        p2p_pack_async(h, PACK_SCALED_W, nullptr, s);
+        ++kernels;
+      }
+      trace_mark(h, it, 2, s);
+      Red ru = red_loop(h, CTL_PIPE_NEXT, false, h->gridA);
+      if (haveIf) ru.store_only = 1;
+      prof_mark(h, profile, 4 * it + 0, s);
+      prof_mark(h, profile, 4 * it + 1, s);
+      prof_mark(h, profile, 4 * it + 2, s);
+      with_format(h, [&](auto A) {
+        k_pipe_SU<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x,
+                                               h->r, h->st, ru);
+      });
+      prof_mark(h, profile, 4 * it + 3, s);
+      trace_mark(h, it, 3, s);
+      ++kernels;
+      if (haveIf) {
+        p2p_join(h, s);
+        Red ri = red_loop(h, CTL_PIPE_NEXT, false);
+        const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->gridA);
+        ri.slot_base = h->gridA;
+        ri.total = h->gridA + ig;
+        k_pipe_fixup_p2p<<<ig, kBlock, 0, s>>>(h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx,
+                                               h->ifCoeffs, h->rD, h->r, h->z, h->w, h->w2, h->st,
+                                               ri, h->p2pDesc, h->nIfFaces);
+        ++kernels;
+      }
+      trace_mark(h, it, 4, s);
+    }
+    return kernels;
+  }
+  if (mr && h->p2pOn) {  // halo + the single reduction over NVLink peer memory
+    const bool haveIf = h->nIfFaces > 0;
+    for (int it = 0; it < batch; ++it) {
+      if (haveIf) {
+        p2p_pack_async(h, PACK_SCALED, h->w, s);
+        ++kernels;
+      }
+      prof_mark(h, profile, 4 * it + 0, s);
+      launch_spmv_scaled(h, h->w, h->nv, s);  // overlaps the peers' reduction traffic
+      prof_mark(h, profile, 4 * it + 1, s);
+      ++kernels;
+      if (haveIf) {
+        p2p_join(h, s);
+        k_iface_apply_p2p<<<small_grid(h->nIfCells), kBlock, 0, s>>>(
+            h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx, h->ifCoeffs, h->nv, h->st,
+            h->p2pDesc, h->nIfFaces);
+        ++kernels;
+      }
+      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_PIPE_NEXT, h->st, h->p2pDesc, haveIf ? 1 : 0);
+      prof_mark(h, profile, 4 * it + 2, s);
+      k_pipe_U<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->nv, h->z, h->s, h->p0, h->x, h->r, h->w,
+                                          h->st, red_loop(h, CTL_PIPE_NEXT, false));
+      prof_mark(h, profile, 4 * it + 3, s);
+      kernels += 2;
+    }
+    return kernels;
+  }
   if (!mr && h->fusePipe) {  // one fused pass per iteration (profile: pass slot 1)
     for (int it = 0; it < batch; ++it) {
       prof_mark(h, profile, 4 * it + 0, s);
@@ -934,7 +1197,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   sh->hist = h->hist;
   sh->histCap = h->histCap;
   CUDA_CHECK(cudaMemcpyAsync(h->st, sh, sizeof(State), cudaMemcpyHostToDevice, s));
-  CUDA_CHECK(cudaMemsetAsync(h->ticket, 0, sizeof(unsigned), s));
+  CUDA_CHECK(cudaMemsetAsync(h->ticket, 0, 2 * sizeof(unsigned), s));
   if (pipelined) {
     CUDA_CHECK(cudaMemsetAsync(h->z, 0, sizeof(double) * n, s));
     CUDA_CHECK(cudaMemsetAsync(h->s, 0, sizeof(double) * n, s));
@@ -976,7 +1239,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
           h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx, h->ifCoeffs, h->recvbuf, h->w, h->st);
       ++kernels;
     }
-    k_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->rD, h->r, h->w, h->st, red_of(h, CTL_PIPE_TOP, !mr));
+    k_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->rD, h->r, h->w, h->st, red_loop(h, CTL_PIPE_TOP, !mr));
     ++kernels;
     // multi-rank: the allgather of these sums is issued by the first loop trip (overlapped)
   }
@@ -996,6 +1259,13 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     for (auto& e : h->prof_ev) CUDA_CHECK(cudaEventCreate(&e));
     if (h->graphs[0][1].exec) { cudaGraphExecDestroy(h->graphs[0][1].exec); h->graphs[0][1] = {}; }
     if (h->graphs[1][1].exec) { cudaGraphExecDestroy(h->graphs[1][1].exec); h->graphs[1][1] = {}; }
+  }
+  if (std::getenv("LDU_TRACE") && (int)h->trace.size() < 5 * batch) {
+    h->trace.assign(5 * batch, nullptr);
+    for (auto& e : h->trace) CUDA_CHECK(cudaEventCreate(&e));
+    for (auto& row : h->graphs)
+      for (auto& GG : row)
+        if (GG.exec) { cudaGraphExecDestroy(GG.exec); GG = {}; }
   }
   if (!G.exec || G.batch != batch) {
     if (G.exec) {
@@ -1020,6 +1290,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   long long launched = 0;
   int batches = 0;
   std::vector<float> passT;  // profile: [batch][it][2] elapsed ms
+  std::vector<float> traceT;  // LDU_TRACE: [batch][it < batch-1][5]
   // multi-rank pipelined needs one more loop trip: the decision on r_i is taken by the
   // control kernel after the overlapped allgather of trip i (single rank: in U_{i-1}).
   const long long trips = (long long)maxIter + ((pipelined && mr) ? 1 : 0);
@@ -1032,7 +1303,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
       }
   };
   if (maxIter > 0) {
-    if (tol == 0.0 && !profile) {  // fixed-iteration run: only breakdown / r == 0 stop early
+    if (tol == 0.0 && !profile && h->trace.empty()) {  // fixed iterations: only breakdown / r == 0 stop early
       const long long nb = (trips + batch - 1) / batch;
       for (long long i = 0; i < nb; ++i) CUDA_CHECK(cudaGraphLaunch(gexec, s));
       batches = (int)nb;
@@ -1043,6 +1314,14 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
         CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
         CUDA_CHECK(cudaStreamSynchronize(s));
         if (profile) collect();
+        if (!h->trace.empty() && pipelined && mr)
+          for (int it = 0; it + 1 < batch; ++it) {
+            float a[5];
+            for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&a[k], h->trace[5 * it + k], h->trace[5 * it + k + 1]);
+            cudaEventElapsedTime(&a[4], h->trace[5 * it + 4], h->trace[5 * (it + 1)]);
+            cudaGetLastError();
+            for (int k = 0; k < 5; ++k) traceT.push_back(a[k]);
+          }
         if (sh->done) break;
         if ((long long)batches * batch >= trips + batch) break;  // safety net
       }
@@ -1075,6 +1354,21 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   h->stats.solveMs = ms;
   CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]));
   h->stats.iterMs = ms;
+  if (!h->trace.empty() && pipelined && mr) {  // segments of the real iterations (debug)
+    double seg[5] = {0, 0, 0, 0, 0};
+    int cnt = 0;
+    const int per = batch - 1;
+    for (size_t g = 0; g < traceT.size() / 5; ++g) {
+      const long long trip = (long long)(g / per) * batch + g % per;
+      if (trip < 2 || trip > sh->iter - 1) continue;
+      for (int k = 0; k < 5; ++k) seg[k] += traceT[5 * g + k];
+      ++cnt;
+    }
+    if (cnt)
+      fprintf(stderr, "[ldu trace rank %d] %d iters, us/iter: ctl %.1f pack %.1f SU %.1f fixup %.1f gap %.1f\n",
+              h->rank, cnt, 1e3 * seg[0] / cnt, 1e3 * seg[1] / cnt, 1e3 * seg[2] / cnt,
+              1e3 * seg[3] / cnt, 1e3 * seg[4] / cnt);
+  }
   h->stats.kernels = kernels + launched;
   h->stats.iterations = sh->iter;
   if (profile) {  // passes that did work: trips 0 .. iter-1 (multi-rank pipelined: 1 .. iter)
@@ -1109,6 +1403,119 @@ void release_work(ldu_handle h) {
   h->prof_ev.clear();
 }
 
+// ---------------------------------------------------------------------------------------------
+// NVLink peer-memory setup (collective over the comm): mailbox allocation, CUDA IPC handle and
+// interface-table exchange with NCCL allgathers, peer mappings, the device descriptor.
+// ---------------------------------------------------------------------------------------------
+void p2p_setup(ldu_handle h) {
+  ldu_comm cm = h->comm;
+  const int R = cm->nRanks, me = cm->rank;
+  if (R > kP2PMaxRanks || (int)h->ifaces.size() > kP2PMaxIf)
+    throw Error(LDU_ERR_INVALID_ARG, "peer-memory path supports <= 64 ranks and <= 16 interfaces");
+  cudaStream_t s = h->own_stream;
+  const size_t bytes = MailboxLayout::bytes(h->nIfFaces);
+  h->mailbox = dmalloc<char>(bytes);
+  CUDA_CHECK(cudaMemset(h->mailbox, 0, bytes));
+  // interface index of every packed face
+  std::vector<int> faceIf(std::max(1, h->nIfFaces), 0);
+  for (size_t k = 0; k < h->ifaces.size(); ++k)
+    for (int i = 0; i < h->ifaces[k].nFaces; ++i) faceIf[h->ifaces[k].offset + i] = (int)k;
+  h->ifFaceIf = dmalloc<int>(faceIf.size());
+  CUDA_CHECK(cudaMemcpy(h->ifFaceIf, faceIf.data(), sizeof(int) * faceIf.size(), cudaMemcpyHostToDevice));
+
+  // exchange IPC handles and interface tables: table = [nIf, nIfFaces, (nb, nFaces, off) x 16]
+  constexpr int TW = 2 + 3 * kP2PMaxIf;
+  cudaIpcMemHandle_t mine;
+  CUDA_CHECK(cudaIpcGetMemHandle(&mine, h->mailbox));
+  std::vector<int> tbl(TW, 0);
+  tbl[0] = (int)h->ifaces.size();
+  tbl[1] = h->nIfFaces;
+  for (size_t k = 0; k < h->ifaces.size(); ++k) {
+    tbl[2 + 3 * k] = h->ifaces[k].neighbRank;
+    tbl[3 + 3 * k] = h->ifaces[k].nFaces;
+    tbl[4 + 3 * k] = h->ifaces[k].offset;
+  }
+  char* dbuf = dmalloc<char>((size_t)R * (sizeof(cudaIpcMemHandle_t) + sizeof(int) * TW) + 64);
+  char* dsend = dbuf;
+  char* drecv = dbuf + sizeof(cudaIpcMemHandle_t) + sizeof(int) * TW;
+  const size_t rec = sizeof(cudaIpcMemHandle_t) + sizeof(int) * TW;
+  std::vector<char> hsend(rec), hrecv(rec * R);
+  std::memcpy(hsend.data(), &mine, sizeof(mine));
+  std::memcpy(hsend.data() + sizeof(mine), tbl.data(), sizeof(int) * TW);
+  char* dall = dmalloc<char>(rec * R);
+  CUDA_CHECK(cudaMemcpy(dsend, hsend.data(), rec, cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllGather(dsend, dall, rec, ncclChar, cm->red, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  CUDA_CHECK(cudaMemcpy(hrecv.data(), dall, rec * R, cudaMemcpyDeviceToHost));
+  dfree(dall);
+  dfree(dbuf);
+  (void)drecv;
+
+  P2PDesc d{};
+  d.rank = me;
+  d.nRanks = R;
+  d.nIf = (int)h->ifaces.size();
+  h->peerMailbox.assign(R, nullptr);
+  for (int r = 0; r < R; ++r) {
+    if (r == me) {
+      d.base[r] = h->mailbox;
+      continue;
+    }
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, hrecv.data() + rec * r, sizeof(hd));
+    void* ptr = nullptr;
+    CUDA_CHECK(cudaIpcOpenMemHandle(&ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    h->peerMailbox[r] = static_cast<char*>(ptr);
+    d.base[r] = static_cast<char*>(ptr);
+  }
+  auto peer_tbl = [&](int r) {
+    return reinterpret_cast<const int*>(hrecv.data() + rec * r + sizeof(cudaIpcMemHandle_t));
+  };
+  for (int k = 0; k < d.nIf; ++k) {
+    const DevInterface& it = h->ifaces[k];
+    int ord = 0;  // ordinal of this interface among mine to the same neighbour (pairing, Z22)
+    for (int j = 0; j < k; ++j) ord += h->ifaces[j].neighbRank == it.neighbRank;
+    const int* pt = peer_tbl(it.neighbRank);
+    int found = -1, seen = 0;
+    for (int kk = 0; kk < pt[0]; ++kk)
+      if (pt[2 + 3 * kk] == me && seen++ == ord) {
+        found = kk;
+        break;
+      }
+    if (found < 0 || pt[3 + 3 * found] != it.nFaces)
+      throw Error(LDU_ERR_INVALID_ARG, "interface " + std::to_string(k) +
+                                           ": no matching interface (same face count) on rank " +
+                                           std::to_string(it.neighbRank));
+    d.ifNeighbor[k] = it.neighbRank;
+    d.ifLocalOff[k] = it.offset;
+    d.ifNFaces[k] = it.nFaces;
+    d.ifRemoteOff[k] = pt[4 + 3 * found];
+    d.ifRemoteIdx[k] = found;
+    d.ifRemoteTotal[k] = pt[1];
+  }
+  h->p2pDesc = dmalloc<P2PDesc>(1);
+  CUDA_CHECK(cudaMemcpy(h->p2pDesc, &d, sizeof(d), cudaMemcpyHostToDevice));
+  // every rank's mailbox is mapped before anyone writes into it
+  int* flag = dmalloc<int>(1);
+  NCCL_CHECK(ncclAllReduce(flag, flag, 1, ncclInt, ncclSum, cm->red, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  dfree(flag);
+  h->p2pOn = true;
+}
+
+void p2p_release(ldu_handle h) {
+  for (char* p : h->peerMailbox)
+    if (p) cudaIpcCloseMemHandle(p);
+  h->peerMailbox.clear();
+  dfree(h->mailbox);
+  dfree(h->p2pDesc);
+  dfree(h->ifFaceIf);
+  h->mailbox = nullptr;
+  h->p2pDesc = nullptr;
+  h->ifFaceIf = nullptr;
+  h->p2pOn = false;
+}
+
 // Launch geometry: grid = SMs x resident blocks of the heaviest pass (multiple of the SM count).
 void configure(ldu_handle h) {
   cudaDeviceProp prop;
@@ -1122,10 +1529,19 @@ void configure(ldu_handle h) {
   if (const char* v = std::getenv("LDU_PIPE_FUSE")) h->fusePipe = std::atoi(v) != 0;
   if (const char* v = std::getenv("LDU_CHUNK")) h->chunkK = std::max(256, std::atoi(v) / 256 * 256);
   const long long need = ((long long)h->n + kBlock - 1) / kBlock;
+  // multi-rank: SMs left free for the NCCL kernels that run concurrently with the passes
+  // (only the NCCL fallback launches NCCL kernels inside the iteration loop)
+  int reserve = 0;
+  if (h->comm && h->comm->nRanks > 1) {
+    const char* v = std::getenv("LDU_P2P");
+    if (v && std::atoi(v) == 0) reserve = 4;
+  }
+  if (const char* v = std::getenv("LDU_RESERVE_SMS")) reserve = std::max(0, std::atoi(v));
+  const int sms = std::max(1, prop.multiProcessorCount - reserve);
   auto grid_of = [&](const void* fn) {
     int o = 1;
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kBlock, 0));
-    long long g = (long long)prop.multiProcessorCount * std::max(1, o);
+    long long g = (long long)sms * std::max(1, o);
     return (int)std::max(1LL, std::min(g, need));
   };
   h->grid = grid_of((const void*)k_cg_passB);  // streaming passes
@@ -1258,13 +1674,17 @@ void configure(ldu_handle h) {
   }
   h->maxParts = std::max(h->grid, h->gridA) + 4096;
   h->partials = dmalloc<double>((size_t)kMaxVals * h->maxParts);
-  h->ticket = dmalloc<unsigned>(1);
-  CUDA_CHECK(cudaMemset(h->ticket, 0, sizeof(unsigned)));
+  h->ticket = dmalloc<unsigned>(2);  // [0] reductions, [1] halo pack (may run concurrently)
+  CUDA_CHECK(cudaMemset(h->ticket, 0, 2 * sizeof(unsigned)));
   h->sums = dmalloc<double>(kMaxVals);
   h->gsums = dmalloc<double>((size_t)kMaxVals * std::max(1, h->nRanks));
   CUDA_CHECK(cudaMemset(h->gsums, 0, sizeof(double) * kMaxVals * std::max(1, h->nRanks)));
   h->st = dmalloc<State>(1);
   CUDA_CHECK(cudaMallocHost((void**)&h->st_host, sizeof(State)));
+  if (h->comm && h->comm->nRanks > 1) {
+    const char* v = std::getenv("LDU_P2P");
+    if (!v || std::atoi(v) != 0) p2p_setup(h);
+  }
 }
 
 double stream_triad(int device, long long n, int reps) {
