@@ -1,0 +1,175 @@
+#!/usr/bin/env python
+"""Measurements of the BASELINE.json configs other than the bench.py headline (config 3).
+
+    python scripts/bench_configs.py c1|c2|c5            (1 GPU)
+    torchrun --nproc-per-node N scripts/bench_configs.py c4   (512^3 z-slabs over N GPUs)
+
+Prints one JSON line per measurement (rank 0).  Times are device times (CUDA events on the
+caller's stream, max over ranks); every solve goes through the C ABI.  The oracle is used only
+to check the GPU's iteration counts / iterates on the same inputs (test-infrastructure use).
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import meshgen  # noqa: E402
+
+
+def ev_time(stream, fn, reps=1):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    out = None
+    for _ in range(reps):
+        out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3, out
+
+
+def c1(ldu):
+    """16^3 Poisson to tol 1e-10, both solvers, vs oracle iteration counts."""
+    import oracle
+    s = meshgen.hex_laplacian(16, 16, 16, dirichlet=dict(x0=1.0))
+    A = ldu.LduMatrix.from_system(s)
+    st = torch.cuda.current_stream()
+    A.set_stream(st.cuda_stream)
+    b = torch.from_numpy(s.b).cuda()
+    for name in ("pcg", "pipecg"):
+        fn = A.pcg_solve if name == "pcg" else A.pipecg_solve
+        x = torch.zeros_like(b)
+        fn(b, x, tol=1e-10, maxIter=10000)
+        reps = 50
+
+        def run():
+            x.zero_()
+            return fn(b, x, tol=1e-10, maxIter=10000)
+        t, (stt, it, res) = ev_time(st, run, reps)
+        oit = (oracle.pcg if name == "pcg" else oracle.pipecg)(s, s.b, tol=1e-10, maxIter=10000)[2]
+        print(json.dumps({"config": "c1 16^3 tol 1e-10", "solver": name, "iters": it,
+                          "oracle_iters": oit, "solve_us": 1e6 * t / reps,
+                          "iter_per_s": it * reps / t}), flush=True)
+
+
+def c2(ldu):
+    """icoFoam cavity pressure 1024^2: 20 PISO steps x 2 correctors = 40 warm-started solves,
+    rel-L2 1e-6 (hot path) and the OpenFOAM normFactor criterion."""
+    nx = ny = 1024
+    s = meshgen.cavity_pressure_2d(nx, ny)
+    A = ldu.LduMatrix.from_system(s)
+    st = torch.cuda.current_stream()
+    A.set_stream(st.cuda_stream)
+    rhs = [torch.from_numpy(meshgen.cavity_rhs(nx, ny, t)).cuda() for t in range(20)]
+    for name in ("pcg", "pipecg"):
+        fn = A.pcg_solve if name == "pcg" else A.pipecg_solve
+        for norm, tol in ((ldu.NORM_L2, 1e-6), (ldu.NORM_OPENFOAM, 1e-6)):
+            x = torch.zeros(s.nCells, dtype=torch.float64, device="cuda")
+            its = []
+
+            def seq():
+                x.zero_()
+                for t in range(20):
+                    for corr in range(2):
+                        _, it, _ = fn(rhs[t], x, tol=tol, maxIter=100000, norm=norm)
+                        its.append(it)
+            seq()
+            its.clear()
+            t, _ = ev_time(st, seq)
+            print(json.dumps({"config": "c2 cavity 1024^2, 40 warm-started solves", "solver": name,
+                              "norm": "L2" if norm == ldu.NORM_L2 else "OpenFOAM", "tol": tol,
+                              "total_iters": int(sum(its)), "first_solve_iters": its[0],
+                              "seconds": t, "iter_per_s": sum(its) / t}), flush=True)
+
+
+def c5(ldu, n=200, iters=300):
+    """Irregular (perturbed, RCM-renumbered) mesh on the SELL-32 path, fixed iterations."""
+    import oracle
+    t0 = time.time()
+    s = meshgen.irregular_mesh(n, seed=1505)
+    gen = time.time() - t0
+    A = ldu.LduMatrix.from_system(s)
+    info = A.info()
+    st = torch.cuda.current_stream()
+    A.set_stream(st.cuda_stream)
+    b = torch.from_numpy(s.b).cuda()
+    N, F = s.nCells, s.nFaces
+    for name in ("pcg", "pipecg"):
+        fn = A.pcg_solve if name == "pcg" else A.pipecg_solve
+        x = torch.zeros_like(b)
+        fn(b, x, tol=0.0, maxIter=iters)
+
+        def run():
+            x.zero_()
+            return fn(b, x, tol=0.0, maxIter=iters)
+        t, _ = ev_time(st, run, 3)
+        rate = 3 * iters / t
+        model = (88 if name == "pcg" else 136) * N + 16 * F
+        # parity sample: 5 fixed iterations vs the oracle
+        xs = torch.zeros_like(b)
+        fn(b, xs, tol=0.0, maxIter=5)
+        ox = (oracle.pcg if name == "pcg" else oracle.pipecg)(s, s.b, tol=0.0, maxIter=5)[1]
+        rel = float(np.linalg.norm(xs.cpu().numpy() - ox) / np.linalg.norm(ox))
+        print(json.dumps({"config": f"c5-like irregular {n}^3 base ({N:,} cells, {F:,} faces), RCM",
+                          "layout": info["layout_name"], "solver": name, "iter_per_s": rate,
+                          "effective_gbps_model": rate * model / 1e9, "rel_err_5it_vs_oracle": rel,
+                          "generation_s": gen}), flush=True)
+
+
+def c4(ldu, iters=300):
+    """512^3 z-slabs over N GPUs (torchrun), fixed iterations, both solvers."""
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [ldu.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = ldu.Comm(rank, world, uid[0], local)
+    s = meshgen.hex_laplacian_slab(512, 512, 512, world, rank, dirichlet=dict(x0=1.0))
+    A = ldu.LduMatrix.from_system(s, comm)
+    st = torch.cuda.current_stream()
+    A.set_stream(st.cuda_stream)
+    b = torch.from_numpy(s.b).cuda()
+    del s
+    for name in ("pipecg", "pcg"):
+        fn = A.pcg_solve if name == "pcg" else A.pipecg_solve
+        x = torch.zeros_like(b)
+        fn(b, x, tol=0.0, maxIter=20)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+        def run():
+            x.zero_()
+            return fn(b, x, tol=0.0, maxIter=iters)
+        t, _ = ev_time(st, run, 2)
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            print(json.dumps({"config": "c4 512^3 z-slabs", "n_gpus": world, "solver": name,
+                              "iter_per_s": 2 * iters / float(tt.item())}), flush=True)
+    A.close()
+    if comm is not None:
+        comm.close()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    import paper_1505_07630_b200 as ldu
+    which = sys.argv[1] if len(sys.argv) > 1 else "c1"
+    if which != "c4":
+        torch.cuda.set_device(0)
+    {"c1": c1, "c2": c2, "c4": c4, "c5": c5}[which](ldu)

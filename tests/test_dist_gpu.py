@@ -20,12 +20,17 @@ def _ngpus():
         return 0
 
 
+@pytest.mark.parametrize("mode", ["p2p_fused", "p2p_split", "nccl"])
 @pytest.mark.parametrize("nproc", [2, 4])
-def test_distributed_parity(nproc):
+def test_distributed_parity(nproc, mode):
+    """Peer-memory path (default; fused and split pipelined passes) and the NCCL fallback."""
     if _ngpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
+    env = dict(os.environ)
+    env["LDU_P2P"] = "0" if mode == "nccl" else "1"
+    env["LDU_PIPE_FUSE"] = "0" if mode == "p2p_split" else "1"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29533",
            os.path.join(ROOT, "tests", "dist_worker.py")]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert p.returncode == 0 and "DIST_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
