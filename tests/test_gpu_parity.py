@@ -237,3 +237,33 @@ def test_bench_config_256cube_sampled(ldu, solver):
 def test_stream_triad(ldu):
     g = ldu.stream_triad(0, 1 << 27, 3)
     assert 3000 < g < 9000, g
+
+
+@pytest.mark.parametrize("norm", ["L2", "OpenFOAM"])
+@pytest.mark.parametrize("solver", ["pcg", "pipecg"])
+def test_cavity_piso_sequence_parity(ldu, solver, norm):
+    """Config 2 semantics: warm-started sequence of pressure solves (6 steps x 2 correctors,
+    tol 1e-6) on the 2-D cavity matrix; per-solve iteration counts and the final field match
+    the oracle's sequence (pipelined CG's true-vs-recurrence residual gap included)."""
+    nx = 128
+    sys = meshgen.cavity_pressure_2d(nx, nx)
+    onorm = oracle.NORM_L2 if norm == "L2" else oracle.NORM_OPENFOAM
+    gnorm = ldu.NORM_L2 if norm == "L2" else ldu.NORM_OPENFOAM
+    ofn = oracle.pcg if solver == "pcg" else oracle.pipecg
+    xo = np.zeros(sys.nCells)
+    its_o = []
+    with ldu.LduMatrix.from_system(sys) as A:
+        fn = A.pcg_solve if solver == "pcg" else A.pipecg_solve
+        x = np.zeros(sys.nCells)
+        its = []
+        for t in range(6):
+            b = meshgen.cavity_rhs(nx, nx, t)
+            for c in range(2):
+                st, it, res = fn(b, x, tol=1e-6, maxIter=100000, norm=gnorm)
+                ost, xo, oit, ores = ofn(sys, b, x0=xo, tol=1e-6, maxIter=100000, norm=onorm)
+                assert st == ldu.OK and ost == oracle.OK
+                its.append(it)
+                its_o.append(oit)
+    for a, b_ in zip(its, its_o):
+        assert abs(a - b_) <= max(1, round(0.02 * b_)), (its, its_o)
+    assert rel(x, xo) <= 1e-6
