@@ -189,6 +189,7 @@ struct ldu_handle_s {
   std::vector<char*> peerMailbox;        // IPC-mapped mailboxes of the other ranks
   ldu::P2PDesc* p2pDesc = nullptr;       // device descriptor
   int* ifFaceIf = nullptr;               // [nIfFaces] interface index of each packed face
+  unsigned long long* tbuf = nullptr;    // LDU_TRACE device timestamps
 };
 
 namespace ldu {

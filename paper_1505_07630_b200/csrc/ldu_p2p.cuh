@@ -33,7 +33,8 @@ struct MailboxLayout {
 // Device-resident descriptor (one per handle).
 struct P2PDesc {
   int rank, nRanks, nIf;
-  unsigned long long seqRed, seqHalo;   // last completed sequence numbers (device state)
+  unsigned long long seqRed, seqHalo;   // last consumed sequence numbers (device state)
+  unsigned long long seqHaloSend;       // last sent halo exchange (advanced only by the pack)
   char* base[kP2PMaxRanks];             // mailbox of every rank (own = local pointer)
   int ifNeighbor[kP2PMaxIf];            // peer rank of my interface k
   int ifLocalOff[kP2PMaxIf];            // my packed face offset of interface k
@@ -41,7 +42,23 @@ struct P2PDesc {
   int ifRemoteOff[kP2PMaxIf];           // offset in the peer's recv of its interface back to me
   int ifRemoteIdx[kP2PMaxIf];           // the peer's interface index (its halo flag slot)
   int ifRemoteTotal[kP2PMaxIf];         // the peer's packed interface face count (recv stride)
+  unsigned long long* tbuf;             // LDU_TRACE: [iteration % 256][8] %globaltimer stamps
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// stamp slot `s` of iteration k: mode 0 store, 1 min, 2 max
+__device__ __forceinline__ void tstamp(P2PDesc* d, int k, int s, int mode) {
+  if (!d || !d->tbuf || k < 0) return;
+  unsigned long long* p = d->tbuf + (k & 255) * 8 + s;
+  const unsigned long long t = gtimer();
+  if (mode == 0) *p = t;
+  else if (mode == 1) atomicMax(p, ~t);  // min, stored complemented (buffer zeroed per solve)
+  else atomicMax(p, t);
+}
 
 __device__ __forceinline__ uint64_t* mb_redflag(char* b, int par, int src) {
   return reinterpret_cast<uint64_t*>(b + MailboxLayout::redFlag) + par * kP2PMaxRanks + src;
@@ -66,6 +83,12 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Flag store after ONE preceding __threadfence_system() that already ordered the data: each
+// st.release.sys is its own system-scope release (serialised, several us apiece over NVLink).
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Bounded spin (~4 s at 2 GHz): a lost peer turns into a kernel error, not a hung GPU.
 __device__ __forceinline__ void spin_until_geq(const uint64_t* p, uint64_t seq) {
   const long long t0 = clock64();
@@ -85,8 +108,17 @@ __device__ __forceinline__ void p2p_publish_sums(P2PDesc* d, const double* sums)
 #pragma unroll
     for (int k = 0; k < NV; ++k) dst[k] = sums[k];
   }
-  // the release stores order this thread's data stores before the flags (no full fence needed)
-  for (int r = 0; r < d->nRanks; ++r) st_release_sys(mb_redflag(d->base[r], par, d->rank), seq);
+  __threadfence_system();  // one system fence orders all data stores before every flag
+  for (int r = 0; r < d->nRanks; ++r) st_relaxed_sys(mb_redflag(d->base[r], par, d->rank), seq);
+}
+
+// Raise the halo flags of exchange `seq` on every neighbour (after all blocks' remote stores
+// were fenced at system scope and counted by the caller's ticket).
+__device__ __forceinline__ void p2p_release_halo(P2PDesc* d, uint64_t seq) {
+  const int par = (int)(seq & 1);
+  __threadfence_system();
+  for (int k = 0; k < d->nIf; ++k)
+    st_relaxed_sys(mb_haloflag(d->base[d->ifNeighbor[k]], par, d->ifRemoteIdx[k]), seq);
 }
 
 // Control kernel side: wait for every rank's sums of the next sequence number, sum them in

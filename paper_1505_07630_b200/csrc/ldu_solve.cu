@@ -354,6 +354,7 @@ __global__ void __launch_bounds__(kBlock) k_pipe_SU(Fmt A, const double* __restr
                                                     double* __restrict__ p, double* __restrict__ x,
                                                     double* __restrict__ r, State* st, Red rd) {
   if (st->done) return;
+  if (threadIdx.x == 0) tstamp(rd.p2p, st->k, 2, 1);
   const double a = st->pa, b = st->pb;
   const bool l2 = st->norm == LDU_NORM_L2;
   const double* __restrict__ w = (st->k & 1) ? w1 : w0;
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(kBlock) k_pipe_SU(Fmt A, const double* __restr
     v[1] = fma(wc, u, v[1]);
     v[2] += l2 ? rc * rc : fabs(rc);
   }
+  if (threadIdx.x == 0) tstamp(rd.p2p, st->k, 3, 2);
   finish_reduction<3>(v, rd, st);
 }
 
@@ -400,9 +402,9 @@ __global__ void __launch_bounds__(kBlock) k_pack_p2p(int nIfFaces, const int* __
     beta = st->beta;
     pold = (st->k & 1) ? p0 : p1;
   }
-  const unsigned long long seq = d->seqHalo + 1;
+  const unsigned long long seq = d->seqHaloSend + 1;
   const int par = (int)(seq & 1);
-  if (mode == PACK_SCALED_W) a = (st->k & 1) ? p1 : p0;  // w_i of the fused pipelined pass
+  if (mode == PACK_SCALED_W) a = (st->k & 1) ? p0 : p1;  // w_{i+1} written by the fused pass i
   GRID_STRIDE(i, nIfFaces) {
     const int c = fc[i];
     double v = a[c];
@@ -422,9 +424,8 @@ __global__ void __launch_bounds__(kBlock) k_pack_p2p(int nIfFaces, const int* __
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
-    __threadfence_system();
-    for (int k = 0; k < d->nIf; ++k)
-      st_release_sys(mb_haloflag(d->base[d->ifNeighbor[k]], par, d->ifRemoteIdx[k]), seq);
+    p2p_release_halo(d, seq);
+    d->seqHaloSend = seq;
     *ticket = 0u;
   }
 }
@@ -487,7 +488,9 @@ __global__ void __launch_bounds__(kBlock) k_pipe_fixup_p2p(int nIfCells, const i
                                                            double* w1, State* st, Red rd,
                                                            P2PDesc* d, int nIfFaces) {
   if (st->done) return;
+  if (threadIdx.x == 0) tstamp(d, st->k, 4, 1);
   const double* recv = p2p_wait_halo(d, nIfFaces);
+  if (threadIdx.x == 0) tstamp(d, st->k, 5, 2);
   const double a = st->pa;
   double* __restrict__ wn = (st->k & 1) ? w0 : w1;
   double v[3] = {0.0, 0.0, 0.0};
@@ -500,17 +503,26 @@ __global__ void __launch_bounds__(kBlock) k_pipe_fixup_p2p(int nIfCells, const i
     wn[c] = fma(-a, dn, wn[c]);
     v[1] = fma(-a * dn, rD[c] * r[c], v[1]);
   }
-  finish_reduction<3>(v, rd, st);
+  if (threadIdx.x == 0) tstamp(d, st->k, 6, 2);
+  finish_reduction<3>(v, rd, st);  // last block publishes the iteration's single reduction
+  if (threadIdx.x == 0) tstamp(d, st->k, 7, 2);
 }
 
-// Control step after a peer-memory reduction: wait for every rank's sums, rank-ordered sum.
+// advanceHalo: 0 no halo exchange, 1 this step follows the consumption of one exchange,
+// 2 (fused pipelined) the previous iteration consumed one -- none before the first trip (k = -1)
 __global__ void k_ctl_p2p(int ctl, State* st, P2PDesc* d, int advanceHalo) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (st->done) return;
+  tstamp(d, st->k + 1, 0, 0);
   double s[kMaxVals];
   p2p_gather_sums<kMaxVals>(d, s);
-  if (advanceHalo) d->seqHalo += 1;
+  tstamp(d, st->k + 1, 1, 0);
+  if (advanceHalo == 1 || (advanceHalo == 2 && st->k >= 0)) d->seqHalo += 1;
   run_ctl(ctl, st, s);
+  // fused pipelined: the exchange already sent for this iteration (by the previous fix-up or the
+  // init) will never be consumed once the solve ends here -- retire its sequence number so the
+  // next solve cannot mistake its flag for a fresh one
+  if (advanceHalo == 2 && st->done) d->seqHalo += 1;
 }
 
 // multi-rank control: sum the allgathered per-rank sums in rank order, then run the step.
@@ -968,17 +980,18 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
   long long kernels = 0;
   const bool mr = multi(h);
   if (mr && h->p2pOn && h->fusePipe) {  // fused S+U pass per iteration over peer memory
+    // trip i: ctl_i (alpha_i, beta_i) -> k_pipe_SU over all rows (internal SpMV) -> [join the
+    // halo stream] -> fix-up of the interface rows with exchange i (publishes the iteration's
+    // single reduction) -> fork the pack of exchange i+1 (rD w_{i+1}) onto the halo stream, where
+    // its NVLink stores and fences overlap ctl_{i+1} and the next fused pass.  Exchange 0 is sent
+    // by the init; every batch ends joined.
     const bool haveIf = h->nIfFaces > 0;
     for (int it = 0; it < batch; ++it) {
       trace_mark(h, it, 0, s);
-      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_PIPE_NEXT, h->st, h->p2pDesc, haveIf ? 1 : 0);
+      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_PIPE_NEXT, h->st, h->p2pDesc, haveIf ? 2 : 0);
       trace_mark(h, it, 1, s);
-      ++kernels;
-      if (haveIf) {  // on the halo stream: the NVLink halo send overlaps the bulk pass below
-        p2p_pack_async(h, PACK_SCALED_W, nullptr, s);
-        ++kernels;
-      }
       trace_mark(h, it, 2, s);
+      ++kernels;
       Red ru = red_loop(h, CTL_PIPE_NEXT, false, h->gridA);
       if (haveIf) ru.store_only = 1;
       prof_mark(h, profile, 4 * it + 0, s);
@@ -992,7 +1005,7 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
       trace_mark(h, it, 3, s);
       ++kernels;
       if (haveIf) {
-        p2p_join(h, s);
+        if (it > 0) p2p_join(h, s);
         Red ri = red_loop(h, CTL_PIPE_NEXT, false);
         const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->gridA);
         ri.slot_base = h->gridA;
@@ -1000,10 +1013,12 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
         k_pipe_fixup_p2p<<<ig, kBlock, 0, s>>>(h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx,
                                                h->ifCoeffs, h->rD, h->r, h->z, h->w, h->w2, h->st,
                                                ri, h->p2pDesc, h->nIfFaces);
-        ++kernels;
+        p2p_pack_async(h, PACK_SCALED_W, nullptr, s);
+        kernels += 2;
       }
       trace_mark(h, it, 4, s);
     }
+    if (haveIf) p2p_join(h, s);
     return kernels;
   }
   if (mr && h->p2pOn) {  // halo + the single reduction over NVLink peer memory
@@ -1198,6 +1213,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   sh->histCap = h->histCap;
   CUDA_CHECK(cudaMemcpyAsync(h->st, sh, sizeof(State), cudaMemcpyHostToDevice, s));
   CUDA_CHECK(cudaMemsetAsync(h->ticket, 0, 2 * sizeof(unsigned), s));
+  if (h->tbuf) CUDA_CHECK(cudaMemsetAsync(h->tbuf, 0, sizeof(unsigned long long) * 256 * 8, s));
   if (pipelined) {
     CUDA_CHECK(cudaMemsetAsync(h->z, 0, sizeof(double) * n, s));
     CUDA_CHECK(cudaMemsetAsync(h->s, 0, sizeof(double) * n, s));
@@ -1241,6 +1257,10 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     }
     k_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->rD, h->r, h->w, h->st, red_loop(h, CTL_PIPE_TOP, !mr));
     ++kernels;
+    if (mr && h->p2pOn && h->fusePipe && h->nIfFaces) {  // exchange 0 of the fused loop
+      p2p_pack(h, PACK_SCALED, h->w, s);
+      ++kernels;
+    }
     // multi-rank: the allgather of these sums is issued by the first loop trip (overlapped)
   }
   CUDA_CHECK(cudaGetLastError());
@@ -1260,7 +1280,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     if (h->graphs[0][1].exec) { cudaGraphExecDestroy(h->graphs[0][1].exec); h->graphs[0][1] = {}; }
     if (h->graphs[1][1].exec) { cudaGraphExecDestroy(h->graphs[1][1].exec); h->graphs[1][1] = {}; }
   }
-  if (std::getenv("LDU_TRACE") && (int)h->trace.size() < 5 * batch) {
+  if (const char* tr = std::getenv("LDU_TRACE"); tr && std::atoi(tr) == 1 && (int)h->trace.size() < 5 * batch) {
     h->trace.assign(5 * batch, nullptr);
     for (auto& e : h->trace) CUDA_CHECK(cudaEventCreate(&e));
     for (auto& row : h->graphs)
@@ -1354,6 +1374,34 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   h->stats.solveMs = ms;
   CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]));
   h->stats.iterMs = ms;
+  if (h->tbuf && pipelined && mr && sh->iter > 20) {  // device %globaltimer stamps (debug)
+    std::vector<unsigned long long> tb(256 * 8);
+    CUDA_CHECK(cudaMemcpy(tb.data(), h->tbuf, sizeof(unsigned long long) * tb.size(), cudaMemcpyDeviceToHost));
+    double acc[8] = {0};
+    int cnt = 0;
+    for (int k = 5; k < std::min(sh->iter - 2, 250); ++k) {
+      unsigned long long a[8], nx[8];
+      for (int q = 0; q < 8; ++q) {
+        a[q] = tb[k * 8 + q];
+        nx[q] = tb[(k + 1) * 8 + q];
+      }
+      a[2] = ~a[2];  // min slots are stored complemented
+      a[4] = ~a[4];
+      acc[0] += (double)(a[1] - a[0]);   // ctl: gather wait
+      acc[1] += (double)(a[2] - a[1]);   // ctl end -> SU first block
+      acc[2] += (double)(a[3] - a[2]);   // SU
+      acc[3] += (double)(a[4] - a[3]);   // SU last block -> fixup first block
+      acc[4] += (double)(a[5] - a[4]);   // fixup halo wait
+      acc[5] += (double)(a[6] - a[5]);   // fixup work
+      acc[6] += (double)(a[7] - a[6]);   // fixup fence + reduction + publish
+      acc[7] += (double)(nx[0] - a[7]);  // -> next ctl start
+      ++cnt;
+    }
+    if (cnt)
+      fprintf(stderr, "[ldu gtimer rank %d] us: ctlwait %.1f ->SU %.1f SU %.1f ->fix %.1f fixwait %.1f fixwork %.1f fixfin %.1f ->ctl %.1f\n",
+              h->rank, acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3,
+              acc[4] / cnt / 1e3, acc[5] / cnt / 1e3, acc[6] / cnt / 1e3, acc[7] / cnt / 1e3);
+  }
   if (!h->trace.empty() && pipelined && mr) {  // segments of the real iterations (debug)
     double seg[5] = {0, 0, 0, 0, 0};
     int cnt = 0;
@@ -1492,6 +1540,10 @@ void p2p_setup(ldu_handle h) {
     d.ifRemoteOff[k] = pt[4 + 3 * found];
     d.ifRemoteIdx[k] = found;
     d.ifRemoteTotal[k] = pt[1];
+  }
+  if (const char* tr = std::getenv("LDU_TRACE"); tr && std::atoi(tr) == 2) {
+    h->tbuf = dmalloc<unsigned long long>(256 * 8);
+    d.tbuf = h->tbuf;
   }
   h->p2pDesc = dmalloc<P2PDesc>(1);
   CUDA_CHECK(cudaMemcpy(h->p2pDesc, &d, sizeof(d), cudaMemcpyHostToDevice));

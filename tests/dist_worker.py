@@ -51,10 +51,17 @@ def main():
         out = {"amul": y.cpu().numpy()}
         b = torch.from_numpy(g.b[lo:hi].copy()).cuda()
         for solver in ("pcg", "pipecg"):
-            x = torch.zeros_like(b)
             fn = A.pcg_solve if solver == "pcg" else A.pipecg_solve
+            # back-to-back solves on one handle (fixed-iteration, converged, warm restart)
+            xw = torch.zeros_like(b)
+            fn(b, xw, tol=0.0, maxIter=7)
+            fn(b, xw, tol=1e-10, maxIter=5000)
+            x = torch.zeros_like(b)
             st, it, res = fn(b, x, tol=1e-10, maxIter=5000)
             stats = A.stats()
+            x2 = torch.zeros_like(b)
+            st2, it2, _ = fn(b, x2, tol=1e-10, maxIter=5000)
+            assert st2 == st and it2 == it and torch.equal(x2, x), "repeat solve differs"
             out[solver] = (st, it, res, x.cpu().numpy(), stats["allreduces"])
         A.close()
         gathered = [None] * world
