@@ -357,3 +357,55 @@ def hex_laplacian_slab(nx: int, ny: int, nz: int, p: int, g: int, **kw) -> LduSy
     loc.meta.update(kind="hex", nx=nx, ny=ny, nz=nz, rank=g, nranks=p, cell_lo=z0 * plane,
                     cell_hi=(z0 + nzl) * plane)
     return loc
+
+
+# --------------------------------------------------------------------------------------------
+# heterogeneous decomposition (Eq 5-8)
+# --------------------------------------------------------------------------------------------
+
+def speed(n_i: int, o_i: int, T: float) -> float:
+    """Eq 5: s_i(n_i) = (n_i + 2 o_i) / T(n_i) -- non-zeros of the local matrix
+    (n_i rows, o_i upper-triangle off-diagonals) per second of one CG iteration."""
+    if T <= 0:
+        raise ValueError("T must be > 0")
+    return (n_i + 2 * o_i) / T
+
+
+def relative_speeds(s) -> np.ndarray:
+    """Eq 6, index collision read as r_i = s_i / sum_j s_j (reading Z14)."""
+    s = np.asarray(s, dtype=F64)
+    if s.size == 0 or np.any(s <= 0):
+        raise ValueError("speeds must be positive")
+    return s / s.sum()
+
+
+def rebalance(N: int, r) -> np.ndarray:
+    """Eq 7-8: n_i,new = N r_i, rounded by largest remainder so that
+    sum_i n_i,new = N exactly (Eq 7)."""
+    r = np.asarray(r, dtype=F64)
+    if r.size == 0 or np.any(r < 0) or abs(r.sum() - 1.0) > 1e-9:
+        raise ValueError("fractions must be >= 0 and sum to 1")
+    raw = N * r
+    n = np.floor(raw).astype(np.int64)
+    rem = int(N - n.sum())
+    order = np.argsort(-(raw - n), kind="stable")  # ties: lowest index first
+    n[order[:rem]] += 1
+    return n
+
+
+def slab_bounds_weighted(nCells: int, fractions) -> np.ndarray:
+    """Contiguous slabs whose sizes follow Eq 8 for the given work fractions (the weights the
+    paper hands to MeTiS/SCOTCH)."""
+    n = rebalance(nCells, fractions)
+    return np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
+
+
+def nnz_balanced_bounds(sys: LduSystem, p: int) -> np.ndarray:
+    """Slab bounds with (nearly) equal local non-zeros n_i + 2 o_i instead of equal cells -- the
+    static estimate of Eq 5 for identical devices on irregular meshes (config 5)."""
+    N = sys.nCells
+    w = np.ones(N) + np.bincount(sys.lowerAddr, minlength=N) + np.bincount(sys.upperAddr, minlength=N)
+    cw = np.concatenate([[0.0], np.cumsum(w)])
+    targets = cw[-1] * np.arange(1, p) / p
+    cuts = np.searchsorted(cw, targets, side="left")
+    return np.concatenate([[0], cuts, [N]]).astype(np.int64)
