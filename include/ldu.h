@@ -142,7 +142,11 @@ typedef struct {
   int batch;         /* iterations per CUDA-graph launch; 0 = library default                   */
   int profile;       /* 1: bracket each pass kernel with CUDA events inside the graph and report
                         per-pass device time in ldu_solve_stats.passMs (one host sync per batch) */
-  int reserved[4];   /* must be zero                                                            */
+  int minIter;       /* OpenFOAM minIter: the stopping test cannot pass before minIter x-updates
+                        (maxIter still ends the solve, NOT_CONVERGED; reading Z26)            */
+  int reserved;      /* must be zero                                                            */
+  double relTol;     /* OpenFOAM relTol: also converged when res < relTol * res0 (0 = off, Z26)  */
+  double reserved2[2]; /* must be zero                                                          */
 } ldu_solve_opts;
 
 ldu_status pcg_solve_ex(ldu_handle h, const double *b, double *x, double tol, int maxIter,

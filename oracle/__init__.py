@@ -50,9 +50,9 @@ def _load():
         lib.oracle_amul.restype = None
         lib.oracle_iface.argtypes = [I, P, P, P, P]
         lib.oracle_iface.restype = None
-        lib.oracle_pcg.argtypes = [I, I, P, P, P, P, P, P, P, D, I, I, P, P, P]
+        lib.oracle_pcg.argtypes = [I, I, P, P, P, P, P, P, P, D, I, I, P, P, P, D, I]
         lib.oracle_pcg.restype = I
-        lib.oracle_pipecg.argtypes = [I, I, P, P, P, P, P, P, P, D, I, I, I, P, P, P]
+        lib.oracle_pipecg.argtypes = [I, I, P, P, P, P, P, P, P, D, I, I, I, P, P, P, D, I]
         lib.oracle_pipecg.restype = I
         _lib = lib
     return _lib
@@ -113,7 +113,8 @@ def dist_amul(parts: Sequence, xs: Sequence[np.ndarray]) -> List[np.ndarray]:
 
 
 def pcg(sys, b: np.ndarray, x0: Optional[np.ndarray] = None, tol: float = 1e-10,
-        maxIter: int = 10000, norm: int = NORM_L2, history: bool = False):
+        maxIter: int = 10000, norm: int = NORM_L2, history: bool = False, relTol: float = 0.0,
+        minIter: int = 0):
     """Jacobi-PCG.  Returns (status, x, nIter, finalRes[, hist])."""
     lib = _load()
     l, u, d, lo, up = _arrays(sys)
@@ -123,14 +124,16 @@ def pcg(sys, b: np.ndarray, x0: Optional[np.ndarray] = None, tol: float = 1e-10,
     res = ctypes.c_double(0.0)
     hist = np.full(maxIter + 1, np.nan) if history else None
     st = lib.oracle_pcg(sys.nCells, l.shape[0], _p(l), _p(u), _p(d), _p(lo), _p(up), _p(bb),
-                        _p(x), tol, maxIter, norm, ctypes.byref(it), ctypes.byref(res), _p(hist))
+                        _p(x), tol, maxIter, norm, ctypes.byref(it), ctypes.byref(res), _p(hist),
+                        relTol, minIter)
     if history:
         return st, x, it.value, res.value, hist[: it.value + 1]
     return st, x, it.value, res.value
 
 
 def pipecg(sys, b: np.ndarray, x0: Optional[np.ndarray] = None, tol: float = 1e-10,
-           maxIter: int = 10000, norm: int = NORM_L2, mode: int = JACOBI, history: bool = False):
+           maxIter: int = 10000, norm: int = NORM_L2, mode: int = JACOBI, history: bool = False,
+           relTol: float = 0.0, minIter: int = 0):
     """Ghysels-Vanroose pipelined CG (mode LITERAL or JACOBI).  Returns like ``pcg``."""
     lib = _load()
     l, u, d, lo, up = _arrays(sys)
@@ -141,7 +144,7 @@ def pipecg(sys, b: np.ndarray, x0: Optional[np.ndarray] = None, tol: float = 1e-
     hist = np.full(maxIter + 1, np.nan) if history else None
     st = lib.oracle_pipecg(sys.nCells, l.shape[0], _p(l), _p(u), _p(d), _p(lo), _p(up), _p(bb),
                            _p(x), tol, maxIter, norm, mode, ctypes.byref(it), ctypes.byref(res),
-                           _p(hist))
+                           _p(hist), relTol, minIter)
     if history:
         return st, x, it.value, res.value, hist[: it.value + 1]
     return st, x, it.value, res.value

@@ -117,16 +117,26 @@ static double crit_eval(const crit_t *cr, int n, const double *r)
     return sum_abs(n, r) / cr->scale;
 }
 
-/* Converged: res < tol (reading Z2), or r is exactly zero (an exact solution; reading Z2'). */
-static int converged(double res, double tol) { return res < tol || res == 0.0; }
+/* Stopping test (readings Z2, Z2', Z26): after `it` x-updates the solve stops when it >= minIter
+ * and (res < tol, or r is exactly zero, or relTol > 0 and res < relTol * res0) -- OpenFOAM's
+ * checkConvergence with its relTol and minIter controls. */
+typedef struct { double tol, relTol, res0; int minIter; } stop_t;
+static int converged(const stop_t *sp, double res, int it)
+{
+    if (it < sp->minIter) return 0;
+    return res < sp->tol || res == 0.0 || (sp->relTol > 0.0 && res < sp->relTol * sp->res0);
+}
 
 /* ---- classical Jacobi-PCG (OpenFOAM PCG order) -------------------------- */
 
 int oracle_pcg(int n, int nf, const int *l, const int *u, const double *diag,
                const double *lower, const double *upper, const double *b, double *x,
-               double tol, int maxIter, int norm, int *nIter, double *finalRes, double *hist)
+               double tol, int maxIter, int norm, int *nIter, double *finalRes, double *hist,
+               double relTol, int minIter)
 {
-    if (n <= 0 || nf < 0 || maxIter < 0 || !b || !x || !diag) return OR_ERR_ARG;
+    if (n <= 0 || nf < 0 || maxIter < 0 || !b || !x || !diag || relTol < 0 || minIter < 0)
+        return OR_ERR_ARG;
+    stop_t sp = {tol, relTol, 0.0, minIter};
     ldu_t A = {n, nf, l, u, diag, lower, upper};
     size_t bytes = sizeof(double) * (size_t)n;
     double *r = malloc(bytes), *z = malloc(bytes), *p = malloc(bytes), *q = malloc(bytes);
@@ -146,9 +156,10 @@ int oracle_pcg(int n, int nf, const int *l, const int *u, const double *diag,
         goto out;
     }
     double res = crit_eval(&cr, n, r);
+    sp.res0 = res;
     if (hist) hist[0] = res;
     *nIter = 0; *finalRes = res;
-    if (converged(res, tol)) { status = OR_OK; goto out; }
+    if (converged(&sp, res, 0)) { status = OR_OK; goto out; }
 
     double rho_old = 0.0;
     for (int k = 0; k < maxIter; ++k) {
@@ -171,7 +182,7 @@ int oracle_pcg(int n, int nf, const int *l, const int *u, const double *diag,
         res = crit_eval(&cr, n, r);
         *nIter = k + 1; *finalRes = res;
         if (hist) hist[k + 1] = res;
-        if (converged(res, tol)) { status = OR_OK; goto out; }
+        if (converged(&sp, res, k + 1)) { status = OR_OK; goto out; }
         rho_old = rho;
     }
     status = OR_NOT_CONVERGED;
@@ -185,10 +196,12 @@ out:
 int oracle_pipecg(int n, int nf, const int *l, const int *u, const double *diag,
                   const double *lower, const double *upper, const double *b, double *x,
                   double tol, int maxIter, int norm, int mode, int *nIter, double *finalRes,
-                  double *hist)
+                  double *hist, double relTol, int minIter)
 {
-    if (n <= 0 || nf < 0 || maxIter < 0 || !b || !x || !diag || (mode != 0 && mode != 1))
+    if (n <= 0 || nf < 0 || maxIter < 0 || !b || !x || !diag || (mode != 0 && mode != 1) ||
+        relTol < 0 || minIter < 0)
         return OR_ERR_ARG;
+    stop_t sp = {tol, relTol, 0.0, minIter};
     ldu_t A = {n, nf, l, u, diag, lower, upper};
     size_t bytes = sizeof(double) * (size_t)n;
     double *r = malloc(bytes), *uu = malloc(bytes), *w = malloc(bytes), *m = malloc(bytes);
@@ -219,9 +232,10 @@ int oracle_pipecg(int n, int nf, const int *l, const int *u, const double *diag,
         double gamma = dot(n, r, uu);
         double delta = dot(n, w, uu);
         double res = crit_eval(&cr, n, r);
+        if (i == 0) sp.res0 = res;
         if (hist) hist[i] = res;
         *nIter = i; *finalRes = res;
-        if (converged(res, tol)) { status = OR_OK; goto out; }
+        if (converged(&sp, res, i)) { status = OR_OK; goto out; }
         if (i == maxIter) { status = OR_NOT_CONVERGED; goto out; }
 
         for (int c = 0; c < n; ++c) m[c] = rD[c] * w[c];      /* m = M^-1 w */

@@ -51,7 +51,8 @@ class _Interfaces(ctypes.Structure):
 
 class SolveOpts(ctypes.Structure):
     _fields_ = [("norm", ctypes.c_int), ("recordHistory", ctypes.c_int), ("batch", ctypes.c_int),
-                ("profile", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
+                ("profile", ctypes.c_int), ("minIter", ctypes.c_int), ("reserved", ctypes.c_int),
+                ("relTol", ctypes.c_double), ("reserved2", ctypes.c_double * 2)]
 
 
 class SolveStats(ctypes.Structure):
@@ -216,10 +217,12 @@ class LduMatrix:
         _check(_lib.ldu_amul(self.handle, _ptr(x, "f64"), _ptr(y, "f64")))
         return y
 
-    def _solve(self, fn, b, x, tol, maxIter, norm, record_history, batch, profile=False):
+    def _solve(self, fn, b, x, tol, maxIter, norm, record_history, batch, profile=False,
+               relTol=0.0, minIter=0):
         it = _I(0)
         res = _D(0.0)
-        opts = SolveOpts(norm, 1 if record_history else 0, batch, 1 if profile else 0)
+        opts = SolveOpts(norm, 1 if record_history else 0, batch, 1 if profile else 0,
+                         int(minIter), 0, float(relTol))
         st = fn(self.handle, _ptr(b, "f64"), _ptr(x, "f64"), float(tol), int(maxIter),
                 ctypes.byref(opts), ctypes.byref(it), ctypes.byref(res))
         if st < 0:
@@ -227,16 +230,18 @@ class LduMatrix:
         return st, it.value, res.value
 
     def pcg_solve(self, b, x, tol: float = 1e-10, maxIter: int = 10000, norm: int = NORM_L2,
-                  record_history: bool = False, batch: int = 0, profile: bool = False):
+                  record_history: bool = False, batch: int = 0, profile: bool = False,
+                  relTol: float = 0.0, minIter: int = 0):
         """Jacobi-PCG; x is in/out.  Returns (status, nIter, finalRes)."""
         return self._solve(_lib.pcg_solve_ex, b, x, tol, maxIter, norm, record_history, batch,
-                           profile)
+                           profile, relTol, minIter)
 
     def pipecg_solve(self, b, x, tol: float = 1e-10, maxIter: int = 10000, norm: int = NORM_L2,
-                     record_history: bool = False, batch: int = 0, profile: bool = False):
+                     record_history: bool = False, batch: int = 0, profile: bool = False,
+                     relTol: float = 0.0, minIter: int = 0):
         """Ghysels-Vanroose pipelined CG; x is in/out.  Returns (status, nIter, finalRes)."""
         return self._solve(_lib.pipecg_solve_ex, b, x, tol, maxIter, norm, record_history, batch,
-                           profile)
+                           profile, relTol, minIter)
 
     def history(self):
         import numpy as np

@@ -67,6 +67,9 @@ struct SellView {
 struct State {
   // per-solve inputs
   double tol;
+  double relTol;     // OpenFOAM relTol (0 = off)
+  double res0;       // criterion value of r0
+  int minIter;       // OpenFOAM minIter
   int maxIter;
   int norm;          // LDU_NORM_*
   int record;        // record history

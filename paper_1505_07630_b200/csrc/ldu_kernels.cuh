@@ -118,7 +118,11 @@ __device__ __forceinline__ void sum_partials(const double* partials, int ld, int
 // ---------------------------------------------------------------------------------------------
 // control steps (one thread; readings Z1-Z3, Z19)
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ bool converged(double res, double tol) { return res < tol || res == 0.0; }
+// stopping test after `it` x-updates (readings Z2, Z2', Z26)
+__device__ __forceinline__ bool converged(const State* st, double res, int it) {
+  if (it < st->minIter) return false;
+  return res < st->tol || res == 0.0 || (st->relTol > 0.0 && res < st->relTol * st->res0);
+}
 
 __device__ __forceinline__ double crit_value(const State* st, double v) {
   return st->norm == LDU_NORM_L2 ? sqrt(v) / st->scale : v / st->scale;
@@ -155,13 +159,14 @@ __device__ __forceinline__ void ctl_cg_init(State* st, const double* s) {
   if (st->done) return;
   const double res = crit_value(st, s[2]);
   record(st, 0, res);
+  st->res0 = res;
   st->iter = 0;
   st->k = 0;
   st->rho = s[1];
   st->alpha = 0.0;
   st->beta = 0.0;
   st->xpending = 0;
-  if (converged(res, st->tol)) finish(st, LDU_OK, 0);
+  if (converged(st, res, 0)) finish(st, LDU_OK, 0);
   else if (st->maxIter == 0) finish(st, LDU_NOT_CONVERGED, 0);
 }
 
@@ -183,7 +188,7 @@ __device__ __forceinline__ void ctl_cg_B(State* st, const double* s) {
   st->xpending = 1;  // alpha_k p_k still to be added to x
   const double res = crit_value(st, s[1]);
   record(st, it, res);
-  if (converged(res, st->tol)) finish(st, LDU_OK, it);
+  if (converged(st, res, it)) finish(st, LDU_OK, it);
   else if (it >= st->maxIter) finish(st, LDU_NOT_CONVERGED, it);
   else {
     st->beta = s[0] / st->rho;
@@ -197,8 +202,9 @@ __device__ __forceinline__ void ctl_pipe_top(State* st, const double* s) {
   const int i = st->k;
   const double res = crit_value(st, s[2]);
   record(st, i, res);
+  if (i == 0) st->res0 = res;
   st->iter = i;
-  if (converged(res, st->tol)) { finish(st, LDU_OK, i); return; }
+  if (converged(st, res, i)) { finish(st, LDU_OK, i); return; }
   if (i >= st->maxIter) { finish(st, LDU_NOT_CONVERGED, i); return; }
   const double g = s[0], d = s[1];
   double a, b;

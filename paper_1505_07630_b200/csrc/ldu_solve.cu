@@ -1155,9 +1155,11 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   ldu_solve_opts o{};
   if (opts) {
     o = *opts;
-    for (int v : o.reserved)
-      if (v) fail_arg("ldu_solve_opts.reserved must be zero");
+    if (o.reserved || o.reserved2[0] != 0.0 || o.reserved2[1] != 0.0)
+      fail_arg("ldu_solve_opts.reserved must be zero");
   }
+  if (!(o.relTol >= 0.0)) fail_arg("relTol must be >= 0");
+  if (o.minIter < 0) fail_arg("minIter must be >= 0");
   if (o.norm != LDU_NORM_L2 && o.norm != LDU_NORM_OPENFOAM) fail_arg("unknown norm");
   if (o.batch < 0) fail_arg("batch must be >= 0");
   if (o.profile != 0 && o.profile != 1) fail_arg("profile must be 0 or 1");
@@ -1206,6 +1208,8 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   State* sh = h->st_host;
   std::memset(sh, 0, sizeof(State));
   sh->tol = tol;
+  sh->relTol = o.relTol;
+  sh->minIter = o.minIter;
   sh->maxIter = maxIter;
   sh->norm = o.norm;
   sh->record = o.recordHistory ? 1 : 0;

@@ -267,3 +267,23 @@ def test_cavity_piso_sequence_parity(ldu, solver, norm):
     for a, b_ in zip(its, its_o):
         assert abs(a - b_) <= max(1, round(0.02 * b_)), (its, its_o)
     assert rel(x, xo) <= 1e-6
+
+
+@pytest.mark.parametrize("solver", ["pcg", "pipecg"])
+def test_reltol_miniter_parity(ldu, solver):
+    """OpenFOAM relTol / minIter (reading Z26) through the C ABI vs the oracle."""
+    sys = meshgen.cavity_pressure_2d(48, 40)
+    b = meshgen.cavity_rhs(48, 40, 2)
+    ofn = oracle.pcg if solver == "pcg" else oracle.pipecg
+    with ldu.LduMatrix.from_system(sys) as A:
+        fn = A.pcg_solve if solver == "pcg" else A.pipecg_solve
+        for kw in (dict(tol=1e-14, relTol=0.05), dict(tol=1e-14, relTol=0.5),
+                   dict(tol=1e300, minIter=9), dict(tol=1e-6, relTol=0.05, minIter=3),
+                   dict(tol=1e300, minIter=50, maxIter=20)):
+            kw = dict(kw)
+            maxIter = kw.pop("maxIter", 5000)
+            ost, ox, oit, ores = ofn(sys, b, maxIter=maxIter, norm=oracle.NORM_OPENFOAM, **kw)
+            x = np.zeros(sys.nCells)
+            st, it, res = fn(b, x, maxIter=maxIter, norm=ldu.NORM_OPENFOAM, **kw)
+            assert st == ost and it == oit, (kw, st, ost, it, oit)
+            assert rel(x, ox) <= 1e-10

@@ -250,3 +250,24 @@ def test_table2_iteration_ratio():
         assert st == oracle.OK
         its.append(it)
     assert 1.8 <= its[1] / its[0] <= 2.1, its
+
+
+@pytest.mark.parametrize("solver", ["pcg", "pipecg_j"])
+def test_reltol_and_miniter(solver):
+    """OpenFOAM relTol / minIter (reading Z26): the solve stops at the FIRST iteration i >= minIter
+    whose criterion value is below tol or below relTol * res0 -- checked against the residual
+    history of an unstopped run (tol = 0), and minIter forces iterations past convergence."""
+    sys = meshgen.cavity_pressure_2d(24, 20)
+    b = meshgen.cavity_rhs(24, 20, 1)
+    f = _solver(solver)
+    _, _, _, _, h = f(sys, b, tol=0.0, maxIter=200, history=True)
+    for relTol in (0.5, 0.05, 1e-3):
+        first = int(np.argmax(h < relTol * h[0]))
+        st, x, it, res = f(sys, b, tol=1e-14, maxIter=200, relTol=relTol)
+        assert st == oracle.OK and it == first and res == h[first]
+    # minIter: a huge tol passes at iteration 0 unless minIter forces more iterations
+    st, x, it, res = f(sys, b, tol=1e300, maxIter=200)
+    assert st == oracle.OK and it == 0
+    st, x, it, res = f(sys, b, tol=1e300, maxIter=200, minIter=7)
+    _, x7, it7, _ = f(sys, b, tol=0.0, maxIter=7)
+    assert st == oracle.OK and it == 7 and np.array_equal(x, x7)
