@@ -155,6 +155,9 @@ struct ldu_handle_s {
   int tT = 0, tTiles = 0, tChunk = 0, tGrid = 0, tL = 1;
   int chunkK = 2048;                  // variant 5: rows per chunk
   bool fusePipe = true;               // single rank: pipelined S+U fused (LDU_PIPE_FUSE)
+  bool persist = false;               // single rank: persistent cooperative kernels
+  int gridP = 0;                      // co-resident grid of the persistent kernels
+  double* ppartials = nullptr;        // [2][kMaxVals][gridP]
   // history
   double* hist = nullptr;
   int histCap = 0;

@@ -22,6 +22,7 @@
 #include "ldu_dia.cuh"
 #include "ldu_march.cuh"
 #include "ldu_tma.cuh"
+#include "ldu_persist.cuh"
 #include "ldu_kernels.cuh"
 
 namespace ldu {
@@ -217,6 +218,67 @@ __global__ void __launch_bounds__(kBlock) k_spmv_scaled_chunk(Fmt A, const doubl
   }
 }
 
+// classical pass A_k, DIA layout with off[0] == 1: the operand p_k at c-1 / c+1 is the
+// neighbouring lane's own value (warp shuffle), as is the coefficient U_0[c-1]; only the lanes at
+// the warp edges load them.  Saves 7 of the ~28 loads per row of the row gather (variant 6).
+template <int ND>
+__global__ void __launch_bounds__(kBlock) k_cg_passA_shfl(DiaView<ND> A,
+                                                          const double* __restrict__ rD,
+                                                          const double* __restrict__ r, double* p0,
+                                                          double* p1, double* __restrict__ q,
+                                                          double* __restrict__ x, State* st,
+                                                          Red rd) {
+  if (st->done) return;
+  const int k = st->k;
+  const double beta = st->beta, alpha = st->alpha;
+  const double* __restrict__ pold = (k & 1) ? p0 : p1;
+  double* __restrict__ pnew = (k & 1) ? p1 : p0;
+  const int lane = threadIdx.x & 31;
+  const int n = A.n;
+  auto op = [&](int j) { return fma(beta, __ldg(pold + j), __ldg(rD + j) * __ldg(r + j)); };
+  double v[1] = {0.0};
+  // whole warps iterate together (shuffles need all lanes); rows >= n are masked
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const int c = base + threadIdx.x;
+    const bool in = c < n;
+    const int cc = in ? c : n - 1;
+    const double po = __ldg(pold + cc);
+    const double rdc = __ldg(rD + cc);
+    const double pc = fma(beta, po, rdc * __ldg(r + cc));
+    const double u0 = __ldg(A.U[0] + cc);
+    double pm = __shfl_up_sync(0xffffffffu, pc, 1);
+    double pp = __shfl_down_sync(0xffffffffu, pc, 1);
+    double um = __shfl_up_sync(0xffffffffu, u0, 1);
+    if (lane == 0) {
+      pm = cc >= 1 ? op(cc - 1) : 0.0;
+      um = cc >= 1 ? __ldg(A.U[0] + cc - 1) : 0.0;
+    }
+    if (lane == 31 || c == n - 1) pp = cc + 1 < n ? op(cc + 1) : 0.0;
+    if (cc < 1) um = 0.0;
+    double s = pc / rdc;
+    // ascending columns: far lower offsets, c-1, c+1, far upper offsets
+#pragma unroll
+    for (int kk = ND - 1; kk >= 1; --kk) {
+      const int j = cc - A.off[kk];
+      if (j >= 0) s = fma(__ldg(A.U[kk] + j), op(j), s);
+    }
+    s = fma(um, pm, s);
+    s = fma(u0, pp, s);
+#pragma unroll
+    for (int kk = 1; kk < ND; ++kk) {
+      const int j = cc + A.off[kk];
+      if (j < n) s = fma(__ldg(A.U[kk] + cc), op(j), s);
+    }
+    if (in) {
+      pnew[c] = pc;
+      q[c] = s;
+      x[c] = fma(alpha, po, x[c]);
+      v[0] = fma(pc, s, v[0]);
+    }
+  }
+  finish_reduction<1>(v, rd, st);
+}
+
 // classical pass A_k, DIA layout, all loads of ROWS rows hoisted (ldu_dia.cuh)
 template <int ND, int ROWS>
 __global__ void __launch_bounds__(kBlock) k_cg_passA_dia(DiaView<ND> A,
@@ -276,6 +338,10 @@ __global__ void __launch_bounds__(kBlock) k_cg_passB(int n, const double* __rest
 // classical exit: x += alpha_k p_k if pending
 __global__ void k_cg_final(int n, const double* p0, const double* p1, double* __restrict__ x,
                            const State* st) {
+  if (st->zero_x) {  // ||b|| = 0 => x = 0 (reading Z1), decided on the device
+    GRID_STRIDE(c, n) x[c] = 0.0;
+    return;
+  }
   if (!st->xpending) return;
   const double alpha = st->alpha;
   const double* __restrict__ p = (st->k & 1) ? p1 : p0;
@@ -716,7 +782,13 @@ void launch_spmv_scaled(ldu_handle h, const double* in, double* out, cudaStream_
 }
 
 void launch_passA(ldu_handle h, const Red& ra, cudaStream_t s) {
-  if (h->variant == 5) {
+  if (h->variant == 6 && h->layout == LDU_LAYOUT_DIA_SYM && h->off[0] == 1) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      k_cg_passA_shfl<ND><<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->r, h->p0, h->p1, h->q, h->x,
+                                                      h->st, ra);
+    });
+  } else if (h->variant == 5) {
     with_format(h, [&](auto A) {
       k_cg_passA_chunk<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->r, h->p0, h->p1, h->q, h->x, h->st, ra,
                                                    h->chunkK);
@@ -1275,6 +1347,83 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   }
   CUDA_CHECK(cudaEventRecord(h->ev[1], s));
 
+  // ---- single rank, persistent cooperative kernel (latency-bound sizes) --------------------
+  if (!mr && h->persist) {
+    if (!h->ppartials) h->ppartials = dmalloc<double>((size_t)2 * kMaxVals * h->gridP);
+    CUDA_CHECK(cudaEventRecord(h->ev[1], s));
+    long long launches = 0;
+    const int trips = tol == 0.0 ? std::max(1, maxIter) : std::max(1, std::min(maxIter, 256));
+    float persistMs = 0.f;
+    if (maxIter > 0) {
+      for (;;) {
+        int ld = h->gridP, mt = trips;
+        void* args[13];
+        int nargs = 0;
+        if (pipelined) {
+          with_format(h, [&](auto A) {
+            using Fmt = decltype(A);
+            static thread_local Fmt Ak;
+            Ak = A;
+            void* a[] = {&Ak, &h->rD, &h->w, &h->w2, &h->z, &h->s, &h->p0, &h->x, &h->r, &h->st,
+                         &h->ppartials, &ld, &mt};
+            nargs = 13;
+            for (int i = 0; i < nargs; ++i) args[i] = a[i];
+            CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+            CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_pipe_persist<Fmt>, h->gridP,
+                                                   kBlock, args, 0, s));
+          });
+        } else {
+          with_format(h, [&](auto A) {
+            using Fmt = decltype(A);
+            static thread_local Fmt Ak;
+            Ak = A;
+            void* a[] = {&Ak, &h->rD, &h->r, &h->p0, &h->p1, &h->q, &h->x, &h->st, &h->ppartials,
+                         &ld, &mt};
+            nargs = 11;
+            for (int i = 0; i < nargs; ++i) args[i] = a[i];
+            CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_cg_persist<Fmt>, h->gridP,
+                                                   kBlock, args, 0, s));
+          });
+        }
+        ++launches;
+        if (tol == 0.0 && trips >= maxIter) break;
+        CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        if (sh->done || launches * (long long)trips > (long long)maxIter + 2) break;
+      }
+    }
+    (void)persistMs;
+    CUDA_CHECK(cudaEventRecord(h->ev[2], s));
+    h->stats.kernels = kernels + launches;
+    // pending x update (classical) / x = 0 when b = 0, on the device: one host sync per solve
+    k_cg_final<<<small_grid(n), kBlock, 0, s>>>(n, h->p0, h->p1, h->x, h->st);
+    ++h->stats.kernels;
+    CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(x, h->x, sizeof(double) * n, xd ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    if (!xd) h->stats.d2hBytes += 8LL * n;
+    CUDA_CHECK(cudaEventRecord(h->ev[3], s));
+    if (h->stream != h->own_stream) {
+      CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+      CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_fork, 0));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[3]));
+    h->stats.solveMs = ms;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]));
+    h->stats.iterMs = ms;
+    h->stats.iterations = sh->iter;
+    if (profile) {  // no per-pass split inside the persistent kernel: whole iterations
+      h->stats.passMs[pipelined ? 1 : 0] = ms;
+      h->stats.passLaunches[pipelined ? 1 : 0] = sh->iter;
+    }
+    if (sh->record) h->histN = std::min(sh->iter + 1, h->histCap);
+    if (!sh->done) sh->status = LDU_NOT_CONVERGED;
+    if (nIter) *nIter = sh->iter;
+    if (finalRes) *finalRes = sh->res;
+    return (ldu_status)sh->status;
+  }
+
   // ---- iteration batches as CUDA graphs ----------------------------------------------------
   ldu_handle_s::Graph& G = h->graphs[pipelined ? 1 : 0][profile ? 1 : 0];
   if (profile && (int)h->prof_ev.size() < 4 * batch) {
@@ -1356,13 +1505,10 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   h->stats.haloBytes += (long long)batches * batch * haloPerIter;
   CUDA_CHECK(cudaEventRecord(h->ev[2], s));
 
-  if (!pipelined) {
-    k_cg_final<<<small_grid(n), kBlock, 0, s>>>(n, h->p0, h->p1, h->x, h->st);
-    ++kernels;
-  }
+  // pending x update (classical) / x = 0 when b = 0, on the device: one host sync per solve
+  k_cg_final<<<small_grid(n), kBlock, 0, s>>>(n, h->p0, h->p1, h->x, h->st);
+  ++kernels;
   CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  if (sh->zero_x) CUDA_CHECK(cudaMemsetAsync(h->x, 0, sizeof(double) * n, s));
   CUDA_CHECK(cudaMemcpyAsync(x, h->x, sizeof(double) * n, xd ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
   if (!xd) h->stats.d2hBytes += 8LL * n;
   CUDA_CHECK(cudaEventRecord(h->ev[3], s));
@@ -1442,6 +1588,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
 
 void release_work(ldu_handle h) {
   for (double** p : {&h->x, &h->r, &h->p0, &h->p1, &h->q, &h->w, &h->w2, &h->nv, &h->z, &h->s,
+                     &h->ppartials,
                      &h->bbuf, &h->ybuf, &h->hist}) {
     dfree(*p);
     *p = nullptr;
@@ -1579,10 +1726,13 @@ void configure(ldu_handle h) {
   // kernel variant of the SpMV-bearing passes (DIA layout): 0 generic, 1 hoisted, 2 hoisted x2
   h->variant = 0;
   if (const char* v = std::getenv("LDU_VARIANT")) h->variant = std::atoi(v);
-  if (h->variant < 0 || h->variant > 5) h->variant = 0;
+  if (h->variant < 0 || h->variant > 6) h->variant = 0;
   h->chunkK = 2048;
   h->fusePipe = true;
   if (const char* v = std::getenv("LDU_PIPE_FUSE")) h->fusePipe = std::atoi(v) != 0;
+  // persistent cooperative kernels for single-rank, latency-bound sizes (LDU_PERSIST=0/1 forces)
+  h->persist = !(h->comm && h->comm->nRanks > 1) && (long long)h->n * 80 < (long long)prop.l2CacheSize;
+  if (const char* v = std::getenv("LDU_PERSIST")) h->persist = std::atoi(v) != 0 && !(h->comm && h->comm->nRanks > 1);
   if (const char* v = std::getenv("LDU_CHUNK")) h->chunkK = std::max(256, std::atoi(v) / 256 * 256);
   const long long need = ((long long)h->n + kBlock - 1) / kBlock;
   // multi-rank: SMs left free for the NCCL kernels that run concurrently with the passes
@@ -1719,6 +1869,12 @@ void configure(ldu_handle h) {
     });
   }
   if (use_tma(h)) h->gridA = h->tGrid;
+  if (h->variant == 6 && h->layout == LDU_LAYOUT_DIA_SYM && h->off[0] == 1) {
+    with_dia(h, [&](auto A) {
+      constexpr int ND = sizeof(A.off) / sizeof(int);
+      h->gridA = grid_of((const void*)k_cg_passA_shfl<ND>);
+    });
+  }
   if (h->variant == 5) {
     with_format(h, [&](auto A) {
       using Fmt = decltype(A);
@@ -1727,6 +1883,16 @@ void configure(ldu_handle h) {
         CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
       h->gridA = grid_of((const void*)k_cg_passA_chunk<Fmt>);
     });
+  }
+  if (h->persist) {  // co-resident grid for the cooperative launches
+    int o1 = 1, o2 = 1;
+    with_format(h, [&](auto A) {
+      using Fmt = decltype(A);
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_pipe_persist<Fmt>, kBlock, 0));
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cg_persist<Fmt>, kBlock, 0));
+    });
+    const long long g = (long long)prop.multiProcessorCount * std::max(1, std::min(o1, o2));
+    h->gridP = (int)std::max(1LL, std::min(g, need));
   }
   h->maxParts = std::max(h->grid, h->gridA) + 4096;
   h->partials = dmalloc<double>((size_t)kMaxVals * h->maxParts);

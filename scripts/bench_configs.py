@@ -88,6 +88,24 @@ def c2(ldu):
                               "norm": "L2" if norm == ldu.NORM_L2 else "OpenFOAM", "tol": tol,
                               "total_iters": int(sum(its)), "first_solve_iters": its[0],
                               "seconds": t, "iter_per_s": sum(its) / t}), flush=True)
+        # icoFoam p / pFinal (NEXT-1): OpenFOAM norm, tol 1e-6, relTol 0.05 then 0 (reading Z26)
+        x = torch.zeros(s.nCells, dtype=torch.float64, device="cuda")
+        its = []
+
+        def piso():
+            x.zero_()
+            for t in range(20):
+                for corr, rt in ((0, 0.05), (1, 0.0)):
+                    _, it, _ = fn(rhs[t], x, tol=1e-6, maxIter=100000, norm=ldu.NORM_OPENFOAM,
+                                  relTol=rt)
+                    its.append(it)
+        piso()
+        its.clear()
+        t, _ = ev_time(st, piso)
+        print(json.dumps({"config": "c2 cavity 1024^2, icoFoam p (relTol 0.05) / pFinal (relTol 0)",
+                          "solver": name, "norm": "OpenFOAM", "tol": 1e-6,
+                          "total_iters": int(sum(its)), "iters_p_pFinal_step0": its[:2],
+                          "seconds": t, "iter_per_s": sum(its) / t}), flush=True)
 
 
 def c5(ldu, n=200, iters=300):

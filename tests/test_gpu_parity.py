@@ -85,9 +85,12 @@ SOLVE_CASES = {
 }
 
 
+@pytest.mark.parametrize("persist", ["0", "1"])
 @pytest.mark.parametrize("solver", ["pcg", "pipecg"])
 @pytest.mark.parametrize("case", sorted(SOLVE_CASES))
-def test_solve_parity(ldu, case, solver):
+def test_solve_parity(ldu, case, solver, persist, monkeypatch):
+    """persist=1: the persistent cooperative kernels; 0: CUDA-graph batches of pass kernels."""
+    monkeypatch.setenv("LDU_PERSIST", persist)
     sys, b = SOLVE_CASES[case]()
     tol = 1e-10
     ofn = oracle.pcg if solver == "pcg" else oracle.pipecg
@@ -110,8 +113,10 @@ def test_solve_parity(ldu, case, solver):
     assert stats["iterations"] == it and stats["kernels"] > 0 and stats["allreduces"] == 0
 
 
+@pytest.mark.parametrize("persist", ["0", "1"])
 @pytest.mark.parametrize("solver", ["pcg", "pipecg"])
-def test_fixed_iterations_track_oracle(ldu, solver):
+def test_fixed_iterations_track_oracle(ldu, solver, persist, monkeypatch):
+    monkeypatch.setenv("LDU_PERSIST", persist)
     """tol = 0 runs exactly maxIter iterations; iterate after k steps matches the oracle's."""
     sys = meshgen.hex_laplacian(24, 20, 18)
     b = meshgen.rhs_hot_face(24, 20, 18)
@@ -127,8 +132,10 @@ def test_fixed_iterations_track_oracle(ldu, solver):
         assert abs(res - ores) <= 1e-9 * ores
 
 
+@pytest.mark.parametrize("persist", ["0", "1"])
 @pytest.mark.parametrize("solver", ["pcg", "pipecg"])
-def test_edge_cases(ldu, solver):
+def test_edge_cases(ldu, solver, persist, monkeypatch):
+    monkeypatch.setenv("LDU_PERSIST", persist)
     sys = meshgen.hex_laplacian(6, 5, 4)
     with ldu.LduMatrix.from_system(sys) as A:
         fn = A.pcg_solve if solver == "pcg" else A.pipecg_solve
@@ -183,7 +190,9 @@ def test_setup_validation(ldu):
         assert ei.value.status == ldu.ERR_INVALID_ARG and msg in str(ei.value)
 
 
-def test_determinism_bitwise(ldu):
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_determinism_bitwise(ldu, persist, monkeypatch):
+    monkeypatch.setenv("LDU_PERSIST", persist)
     sys = meshgen.hex_laplacian(30, 30, 30, conductance_sigma=0.5, seed=2)
     b = meshgen.rhs_random(sys.nCells, 5)
     xs = []

@@ -1,5 +1,5 @@
 """Every SpMV-bearing kernel variant of the DIA layout (LDU_VARIANT: 0 generic row gather,
-1/2 hoisted loads, 3 plane-marching smem ring, 4 TMA-fed plane march) against the oracle, on meshes whose far offset
+1/2 hoisted loads, 3 plane-marching smem ring, 4 TMA-fed plane march, 5 chunked wavefront, 6 warp-shuffle neighbours) against the oracle, on meshes whose far offset
 nx*ny >= 4096 so the marching geometry applies (incl. ragged tiles and a partial last tile)."""
 import os
 
@@ -29,15 +29,18 @@ def ldu():
 
 
 def _make(ldu, sys, variant):
-    old = os.environ.get("LDU_VARIANT")
+    """Variants live in the CUDA-graph pass kernels: force them (no persistent kernel)."""
+    saved = {k: os.environ.get(k) for k in ("LDU_VARIANT", "LDU_PERSIST")}
     os.environ["LDU_VARIANT"] = str(variant)
+    os.environ["LDU_PERSIST"] = "0"
     try:
         return ldu.LduMatrix.from_system(sys)
     finally:
-        if old is None:
-            del os.environ["LDU_VARIANT"]
-        else:
-            os.environ["LDU_VARIANT"] = old
+        for k, v in saved.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
 
 
 @pytest.mark.parametrize("mesh", sorted(MESHES))
@@ -46,7 +49,7 @@ def test_amul_variants_bitwise(ldu, mesh):
     x = np.random.default_rng(4).uniform(-1, 1, sys.nCells)
     yo = oracle.amul(sys, x)
     ys = []
-    for v in (0, 1, 2, 3, 4, 5):
+    for v in (0, 1, 2, 3, 4, 5, 6):
         with _make(ldu, sys, v) as A:
             assert A.info()["layout_name"] == "DIA_SYM"
             y = np.empty(sys.nCells)
@@ -58,7 +61,7 @@ def test_amul_variants_bitwise(ldu, mesh):
 
 
 @pytest.mark.parametrize("solver", ["pcg", "pipecg"])
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("mesh", sorted(MESHES))
 def test_solve_variants(ldu, mesh, variant, solver):
     sys = MESHES[mesh]()
@@ -84,15 +87,17 @@ def test_pipelined_fused_and_split(ldu, mesh, fuse):
     """Single rank: pipelined CG with S and U fused (default) and split (LDU_PIPE_FUSE=0)."""
     sys = MESHES[mesh]()
     ost, ox, oit, ores = oracle.pipecg(sys, sys.b, tol=1e-10, maxIter=5000)
-    old = os.environ.get("LDU_PIPE_FUSE")
+    saved = {k: os.environ.get(k) for k in ("LDU_PIPE_FUSE", "LDU_PERSIST")}
     os.environ["LDU_PIPE_FUSE"] = str(fuse)
+    os.environ["LDU_PERSIST"] = "0"
     try:
         A = ldu.LduMatrix.from_system(sys)
     finally:
-        if old is None:
-            del os.environ["LDU_PIPE_FUSE"]
-        else:
-            os.environ["LDU_PIPE_FUSE"] = old
+        for k, v in saved.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
     with A:
         assert A.info()["pipeFused"] == fuse
         x = np.zeros(sys.nCells)
