@@ -49,6 +49,15 @@ __device__ __forceinline__ double row_apply(const SellView& A, int c, double s, 
 }
 
 // ---------------------------------------------------------------------------------------------
+// programmatic dependent launch (PDL): a kernel launched with programmatic stream serialisation
+// may start while its predecessor drains; it must wait before touching the predecessor's data.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------------------------
 // deterministic reductions
 // ---------------------------------------------------------------------------------------------
 template <int NV>

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <utility>
 #include <cstdlib>
 #include <vector>
 
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(kBlock) k_pipe_SU(Fmt A, const double* __restr
                                                     double* __restrict__ z, double* __restrict__ s,
                                                     double* __restrict__ p, double* __restrict__ x,
                                                     double* __restrict__ r, State* st, Red rd) {
+  pdl_wait();  // launched programmatically after the control step (no-op otherwise)
   if (st->done) return;
   if (threadIdx.x == 0) tstamp(rd.p2p, st->k, 2, 1);
   const double a = st->pa, b = st->pb;
@@ -446,6 +448,7 @@ __global__ void __launch_bounds__(kBlock) k_pipe_SU(Fmt A, const double* __restr
     v[1] = fma(wc, u, v[1]);
     v[2] += l2 ? rc * rc : fabs(rc);
   }
+  pdl_trigger();  // the fix-up may launch now; it waits for this grid before reading
   if (threadIdx.x == 0) tstamp(rd.p2p, st->k, 3, 2);
   finish_reduction<3>(v, rd, st);
 }
@@ -553,6 +556,7 @@ __global__ void __launch_bounds__(kBlock) k_pipe_fixup_p2p(int nIfCells, const i
                                                            double* __restrict__ z, double* w0,
                                                            double* w1, State* st, Red rd,
                                                            P2PDesc* d, int nIfFaces) {
+  pdl_wait();
   if (st->done) return;
   if (threadIdx.x == 0) tstamp(d, st->k, 4, 1);
   const double* recv = p2p_wait_halo(d, nIfFaces);
@@ -577,6 +581,8 @@ __global__ void __launch_bounds__(kBlock) k_pipe_fixup_p2p(int nIfCells, const i
 // advanceHalo: 0 no halo exchange, 1 this step follows the consumption of one exchange,
 // 2 (fused pipelined) the previous iteration consumed one -- none before the first trip (k = -1)
 __global__ void k_ctl_p2p(int ctl, State* st, P2PDesc* d, int advanceHalo) {
+  pdl_wait();
+  pdl_trigger();  // let the fused pass launch and park in pdl_wait while we spin
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (st->done) return;
   tstamp(d, st->k + 1, 0, 0);
@@ -614,6 +620,22 @@ __global__ void k_triad(long long n, double* __restrict__ a, const double* __res
 // ---------------------------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------------------------
+// Launch with programmatic stream serialisation (PDL) when enabled (LDU_PDL, default on).
+template <class... KArgs, class... Args>
+void launch_pdl(bool pdl, void (*kernel)(KArgs...), int grid, int block, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 template <class F>
 void with_format(ldu_handle h, F&& f) {
   if (h->layout == LDU_LAYOUT_SELL32) {
@@ -1060,7 +1082,8 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
     const bool haveIf = h->nIfFaces > 0;
     for (int it = 0; it < batch; ++it) {
       trace_mark(h, it, 0, s);
-      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_PIPE_NEXT, h->st, h->p2pDesc, haveIf ? 2 : 0);
+      const bool pdl = h->pdl && !profile && h->trace.empty() && (it > 0 || !haveIf);
+      launch_pdl(pdl, k_ctl_p2p, 1, 32, s, (int)CTL_PIPE_NEXT, h->st, h->p2pDesc, haveIf ? 2 : 0);
       trace_mark(h, it, 1, s);
       trace_mark(h, it, 2, s);
       ++kernels;
@@ -1070,8 +1093,9 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
       prof_mark(h, profile, 4 * it + 1, s);
       prof_mark(h, profile, 4 * it + 2, s);
       with_format(h, [&](auto A) {
-        k_pipe_SU<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x,
-                                               h->r, h->st, ru);
+        launch_pdl(h->pdl && !profile && h->trace.empty(), k_pipe_SU<decltype(A)>, h->gridA,
+                   kBlock, s, A, (const double*)h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x,
+                   h->r, h->st, ru);
       });
       prof_mark(h, profile, 4 * it + 3, s);
       trace_mark(h, it, 3, s);
@@ -1082,9 +1106,10 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
         const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->gridA);
         ri.slot_base = h->gridA;
         ri.total = h->gridA + ig;
-        k_pipe_fixup_p2p<<<ig, kBlock, 0, s>>>(h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx,
-                                               h->ifCoeffs, h->rD, h->r, h->z, h->w, h->w2, h->st,
-                                               ri, h->p2pDesc, h->nIfFaces);
+        launch_pdl(false, k_pipe_fixup_p2p,  // follows a cross-stream join: plain dependency
+                   ig, kBlock, s, h->nIfCells, (const int*)h->ifCell, (const int*)h->ifCellPtr,
+                   (const int*)h->ifFaceIdx, (const double*)h->ifCoeffs, (const double*)h->rD,
+                   (const double*)h->r, h->z, h->w, h->w2, h->st, ri, h->p2pDesc, h->nIfFaces);
         p2p_pack_async(h, PACK_SCALED_W, nullptr, s);
         kernels += 2;
       }
@@ -1730,6 +1755,8 @@ void configure(ldu_handle h) {
   h->chunkK = 2048;
   h->fusePipe = true;
   if (const char* v = std::getenv("LDU_PIPE_FUSE")) h->fusePipe = std::atoi(v) != 0;
+  h->pdl = true;
+  if (const char* v = std::getenv("LDU_PDL")) h->pdl = std::atoi(v) != 0;
   // persistent cooperative kernels for single-rank, latency-bound sizes (LDU_PERSIST=0/1 forces)
   h->persist = !(h->comm && h->comm->nRanks > 1) && (long long)h->n * 80 < (long long)prop.l2CacheSize;
   if (const char* v = std::getenv("LDU_PERSIST")) h->persist = std::atoi(v) != 0 && !(h->comm && h->comm->nRanks > 1);
