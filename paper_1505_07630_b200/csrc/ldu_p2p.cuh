@@ -42,7 +42,7 @@ struct P2PDesc {
   int ifRemoteOff[kP2PMaxIf];           // offset in the peer's recv of its interface back to me
   int ifRemoteIdx[kP2PMaxIf];           // the peer's interface index (its halo flag slot)
   int ifRemoteTotal[kP2PMaxIf];         // the peer's packed interface face count (recv stride)
-  unsigned long long* tbuf;             // LDU_TRACE: [iteration % 256][8] %globaltimer stamps
+  unsigned long long* tbuf;             // LDU_TRACE: [iteration % 256][16] %globaltimer stamps
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -53,7 +53,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // stamp slot `s` of iteration k: mode 0 store, 1 min, 2 max
 __device__ __forceinline__ void tstamp(P2PDesc* d, int k, int s, int mode) {
   if (!d || !d->tbuf || k < 0) return;
-  unsigned long long* p = d->tbuf + (k & 255) * 8 + s;
+  unsigned long long* p = d->tbuf + (k & 255) * 16 + s;
   const unsigned long long t = gtimer();
   if (mode == 0) *p = t;
   else if (mode == 1) atomicMax(p, ~t);  // min, stored complemented (buffer zeroed per solve)

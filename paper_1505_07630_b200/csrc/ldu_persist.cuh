@@ -24,11 +24,7 @@ template <int NV>
 __device__ __forceinline__ void persist_sum(const double* partials, int ld, int G, double* out) {
   __shared__ double sm[NV][32];
   double v[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    v[k] = 0.0;
-    for (int i = threadIdx.x; i < G; i += blockDim.x) v[k] += __ldcg(partials + k * ld + i);
-  }
+  sum_slots<NV>(partials, ld, G, v);
   block_reduce<NV>(v, sm);
   if (threadIdx.x == 0)
 #pragma unroll

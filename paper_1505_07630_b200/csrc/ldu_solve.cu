@@ -1314,7 +1314,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   sh->histCap = h->histCap;
   CUDA_CHECK(cudaMemcpyAsync(h->st, sh, sizeof(State), cudaMemcpyHostToDevice, s));
   CUDA_CHECK(cudaMemsetAsync(h->ticket, 0, 2 * sizeof(unsigned), s));
-  if (h->tbuf) CUDA_CHECK(cudaMemsetAsync(h->tbuf, 0, sizeof(unsigned long long) * 256 * 8, s));
+  if (h->tbuf) CUDA_CHECK(cudaMemsetAsync(h->tbuf, 0, sizeof(unsigned long long) * 256 * 16, s));
   if (pipelined) {
     CUDA_CHECK(cudaMemsetAsync(h->z, 0, sizeof(double) * n, s));
     CUDA_CHECK(cudaMemsetAsync(h->s, 0, sizeof(double) * n, s));
@@ -1550,15 +1550,15 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]));
   h->stats.iterMs = ms;
   if (h->tbuf && pipelined && mr && sh->iter > 20) {  // device %globaltimer stamps (debug)
-    std::vector<unsigned long long> tb(256 * 8);
+    std::vector<unsigned long long> tb(256 * 16);
     CUDA_CHECK(cudaMemcpy(tb.data(), h->tbuf, sizeof(unsigned long long) * tb.size(), cudaMemcpyDeviceToHost));
-    double acc[8] = {0};
+    double acc[11] = {0};
     int cnt = 0;
     for (int k = 5; k < std::min(sh->iter - 2, 250); ++k) {
-      unsigned long long a[8], nx[8];
-      for (int q = 0; q < 8; ++q) {
-        a[q] = tb[k * 8 + q];
-        nx[q] = tb[(k + 1) * 8 + q];
+      unsigned long long a[16], nx[16];
+      for (int q = 0; q < 16; ++q) {
+        a[q] = tb[k * 16 + q];
+        nx[q] = tb[(k + 1) * 16 + q];
       }
       a[2] = ~a[2];  // min slots are stored complemented
       a[4] = ~a[4];
@@ -1570,12 +1570,16 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
       acc[5] += (double)(a[6] - a[5]);   // fixup work
       acc[6] += (double)(a[7] - a[6]);   // fixup fence + reduction + publish
       acc[7] += (double)(nx[0] - a[7]);  // -> next ctl start
+      acc[8] += (double)(a[8] - a[6]);   // blocks done -> last block past the ticket
+      acc[9] += (double)(a[9] - a[8]);   // sum of partials
+      acc[10] += (double)(a[10] - a[9]); // publish
       ++cnt;
     }
     if (cnt)
-      fprintf(stderr, "[ldu gtimer rank %d] us: ctlwait %.1f ->SU %.1f SU %.1f ->fix %.1f fixwait %.1f fixwork %.1f fixfin %.1f ->ctl %.1f\n",
+      fprintf(stderr, "[ldu gtimer rank %d] us: ctlwait %.1f ->SU %.1f SU %.1f ->fix %.1f fixwait %.1f fixwork %.1f fixfin %.1f (ticket %.1f sum %.1f publish %.1f) ->ctl %.1f\n",
               h->rank, acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3,
-              acc[4] / cnt / 1e3, acc[5] / cnt / 1e3, acc[6] / cnt / 1e3, acc[7] / cnt / 1e3);
+              acc[4] / cnt / 1e3, acc[5] / cnt / 1e3, acc[6] / cnt / 1e3, acc[8] / cnt / 1e3,
+              acc[9] / cnt / 1e3, acc[10] / cnt / 1e3, acc[7] / cnt / 1e3);
   }
   if (!h->trace.empty() && pipelined && mr) {  // segments of the real iterations (debug)
     double seg[5] = {0, 0, 0, 0, 0};
@@ -1718,7 +1722,7 @@ void p2p_setup(ldu_handle h) {
     d.ifRemoteTotal[k] = pt[1];
   }
   if (const char* tr = std::getenv("LDU_TRACE"); tr && std::atoi(tr) == 2) {
-    h->tbuf = dmalloc<unsigned long long>(256 * 8);
+    h->tbuf = dmalloc<unsigned long long>(256 * 16);
     d.tbuf = h->tbuf;
   }
   h->p2pDesc = dmalloc<P2PDesc>(1);
