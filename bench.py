@@ -68,16 +68,22 @@ def pass_model_bytes(solver, N, F, fused=False):
 
 
 def pass_format_bytes(solver, info, N):
-    """Bytes the dominant kernel must move in the layout it actually streams."""
+    """Bytes the dominant kernel(s) must move in the layout actually streamed.
+    Classical pass A with variant 7 is two kernels: A1 (r, rD, p_old, x in; p, x out: 48N) and
+    A2 (p, rD, coefficients in; q out)."""
     if solver == "pipecg":
         if not info.get("pipeFused"):
             return 112 * N
         if info["layout_name"] == "DIA_SYM":  # w, rD, z, s, r, p, x, U_k in; z, s, p, x, r, w out
             return (13 + info["nDiagonals"]) * 8 * N
         return 104 * N + 12 * info["storedEntries"] + 12 * ((N + 31) // 32)
+    split = info.get("variant") == 7
     if info["layout_name"] == "DIA_SYM":
+        if split:
+            return 48 * N + (24 + 8 * info["nDiagonals"]) * N
         return 56 * N + 8 * info["nDiagonals"] * N  # r, rD, p_old, x in; p, q, x out; U_k once
-    return 56 * N + 12 * info["storedEntries"] + 12 * ((N + 31) // 32)
+    base = 48 * N + 24 * N if split else 56 * N
+    return base + 12 * info["storedEntries"] + 12 * ((N + 31) // 32)
 
 
 def hbm_peak():
@@ -334,7 +340,8 @@ def main():
             fused = bool(info.get("pipeFused")) and solver == "pipecg"
             mb = pass_model_bytes(solver, N, F, fused)
             fb = pass_format_bytes(solver, info, N)
-            roof = {"kernel": "k_cg_passA" if solver == "pcg" else ("k_pipe_SU" if fused else "k_pipe_U"),
+            kname = ("k_cg_passA1+k_cg_passA2" if info.get("variant") == 7 else "k_cg_passA")
+            roof = {"kernel": kname if solver == "pcg" else ("k_pipe_SU" if fused else "k_pipe_U"),
                     "bound": "hbm", "achieved": mb / t_launch / 1e9, "peak": peak, "unit": "GB/s",
                     "frac": mb / t_launch / 1e9 / peak, "traffic": ncu_traffic(solver, n, world),
                     "model_bytes_per_launch": mb, "launch_us": t_launch * 1e6,

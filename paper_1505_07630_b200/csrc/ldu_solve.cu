@@ -219,6 +219,42 @@ __global__ void __launch_bounds__(kBlock) k_spmv_scaled_chunk(Fmt A, const doubl
   }
 }
 
+// classical pass A_k split in two (variant 7): A1 streams p_k = rD.r + beta p_{k-1} and
+// x += alpha_{k-1} p_{k-1} (48N bytes); A2 is a plain SpMV q = A p_k gathering one array, with
+// partial (p_k, q) (48N bytes, diag term p / rD).  96N instead of the fused 80N, but no operand
+// recomputation at the neighbours.
+__global__ void __launch_bounds__(kBlock) k_cg_passA1(int n, const double* __restrict__ rD,
+                                                      const double* __restrict__ r, double* p0,
+                                                      double* p1, double* __restrict__ x,
+                                                      const State* st) {
+  if (st->done) return;
+  const int k = st->k;
+  const double beta = st->beta, alpha = st->alpha;
+  const double* __restrict__ pold = (k & 1) ? p0 : p1;
+  double* __restrict__ pnew = (k & 1) ? p1 : p0;
+  GRID_STRIDE(c, n) {
+    const double po = pold[c];
+    pnew[c] = fma(beta, po, rD[c] * r[c]);
+    x[c] = fma(alpha, po, x[c]);
+  }
+}
+
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_cg_passA2(Fmt A, const double* __restrict__ rD,
+                                                      const double* p0, const double* p1,
+                                                      double* __restrict__ q, State* st, Red rd) {
+  if (st->done) return;
+  const double* __restrict__ p = (st->k & 1) ? p1 : p0;
+  double v[1] = {0.0};
+  GRID_STRIDE(c, A.n) {
+    const double pc = __ldg(p + c);
+    const double qc = row_apply(A, c, pc / __ldg(rD + c), [&](int j) { return __ldg(p + j); });
+    q[c] = qc;
+    v[0] = fma(pc, qc, v[0]);
+  }
+  finish_reduction<1>(v, rd, st);
+}
+
 // classical pass A_k, DIA layout with off[0] == 1: the operand p_k at c-1 / c+1 is the
 // neighbouring lane's own value (warp shuffle), as is the coefficient U_0[c-1]; only the lanes at
 // the warp edges load them.  Saves 7 of the ~28 loads per row of the row gather (variant 6).
@@ -804,7 +840,12 @@ void launch_spmv_scaled(ldu_handle h, const double* in, double* out, cudaStream_
 }
 
 void launch_passA(ldu_handle h, const Red& ra, cudaStream_t s) {
-  if (h->variant == 6 && h->layout == LDU_LAYOUT_DIA_SYM && h->off[0] == 1) {
+  if (h->variant == 7) {
+    k_cg_passA1<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->r, h->p0, h->p1, h->x, h->st);
+    with_format(h, [&](auto A) {
+      k_cg_passA2<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->p0, h->p1, h->q, h->st, ra);
+    });
+  } else if (h->variant == 6 && h->layout == LDU_LAYOUT_DIA_SYM && h->off[0] == 1) {
     with_dia(h, [&](auto A) {
       constexpr int ND = sizeof(A.off) / sizeof(int);
       k_cg_passA_shfl<ND><<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->r, h->p0, h->p1, h->q, h->x,
@@ -1753,9 +1794,9 @@ void configure(ldu_handle h) {
   cudaDeviceProp prop;
   CUDA_CHECK(cudaGetDeviceProperties(&prop, h->device));
   // kernel variant of the SpMV-bearing passes (DIA layout): 0 generic, 1 hoisted, 2 hoisted x2
-  h->variant = 0;
+  h->variant = 7;  // measured fastest for classical pass A (profiles/r01_variants)
   if (const char* v = std::getenv("LDU_VARIANT")) h->variant = std::atoi(v);
-  if (h->variant < 0 || h->variant > 6) h->variant = 0;
+  if (h->variant < 0 || h->variant > 7) h->variant = 0;
   h->chunkK = 2048;
   h->fusePipe = true;
   if (const char* v = std::getenv("LDU_PIPE_FUSE")) h->fusePipe = std::atoi(v) != 0;

@@ -1,5 +1,5 @@
 """Every SpMV-bearing kernel variant of the DIA layout (LDU_VARIANT: 0 generic row gather,
-1/2 hoisted loads, 3 plane-marching smem ring, 4 TMA-fed plane march, 5 chunked wavefront, 6 warp-shuffle neighbours) against the oracle, on meshes whose far offset
+1/2 hoisted loads, 3 plane-marching smem ring, 4 TMA-fed plane march, 5 chunked wavefront, 6 warp-shuffle neighbours, 7 split update + SpMV) against the oracle, on meshes whose far offset
 nx*ny >= 4096 so the marching geometry applies (incl. ragged tiles and a partial last tile)."""
 import os
 
@@ -49,7 +49,7 @@ def test_amul_variants_bitwise(ldu, mesh):
     x = np.random.default_rng(4).uniform(-1, 1, sys.nCells)
     yo = oracle.amul(sys, x)
     ys = []
-    for v in (0, 1, 2, 3, 4, 5, 6):
+    for v in (0, 1, 2, 3, 4, 5, 6, 7):
         with _make(ldu, sys, v) as A:
             assert A.info()["layout_name"] == "DIA_SYM"
             y = np.empty(sys.nCells)
@@ -61,7 +61,7 @@ def test_amul_variants_bitwise(ldu, mesh):
 
 
 @pytest.mark.parametrize("solver", ["pcg", "pipecg"])
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("mesh", sorted(MESHES))
 def test_solve_variants(ldu, mesh, variant, solver):
     sys = MESHES[mesh]()
