@@ -17,6 +17,8 @@ MESHES = {
     "70x61x13_sigma": lambda: meshgen.hex_laplacian(70, 61, 13, conductance_sigma=0.7, seed=9,
                                                     dirichlet=dict(x0=1.0)),
     "130x33x5_ddt": lambda: meshgen.hex_laplacian(130, 33, 5, ddt=0.5, dirichlet=dict(z0=2.0)),
+    "96x43x7_sigma": lambda: meshgen.hex_laplacian(96, 43, 7, conductance_sigma=0.4, seed=3,
+                                                   dirichlet=dict(y1=1.0)),
 }
 
 
