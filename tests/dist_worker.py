@@ -63,6 +63,11 @@ def main():
             st2, it2, _ = fn(b, x2, tol=1e-10, maxIter=5000)
             assert st2 == st and it2 == it and torch.equal(x2, x), "repeat solve differs"
             out[solver] = (st, it, res, x.cpu().numpy(), stats["allreduces"])
+            # OpenFOAM normFactor + relTol + minIter + residual history across ranks (Z1, Z26)
+            xo = torch.zeros_like(b)
+            sto, ito, reso = fn(b, xo, tol=1e-6, maxIter=5000, norm=ldu.NORM_OPENFOAM,
+                                relTol=0.01, minIter=3, record_history=True)
+            out[solver + "_of"] = (sto, ito, reso, xo.cpu().numpy(), A.history())
         A.close()
         gathered = [None] * world
         dist.all_gather_object(gathered, out)
@@ -87,6 +92,19 @@ def main():
                 ok &= rel <= 1e-8
                 per_iter = 2 if solver == "pcg" else 1  # reading Z4 / P:97
                 ok &= reds >= per_iter * it
+                # OpenFOAM criterion with relTol / minIter: same stop and history as the oracle
+                ost2, ox2, oit2, ores2, ohist2 = ofn(g, g.b, tol=1e-6, maxIter=5000,
+                                                     norm=oracle.NORM_OPENFOAM, relTol=0.01,
+                                                     minIter=3, history=True)
+                of = [o[solver + "_of"] for o in gathered]
+                x_of = np.concatenate([o[3] for o in of])
+                rel_of = float(np.linalg.norm(x_of - ox2) / np.linalg.norm(ox2))
+                hist = of[0][4]
+                hist_ok = len(hist) == of[0][1] + 1 and np.allclose(hist[:len(ohist2)], ohist2[:len(hist)], rtol=1e-6)
+                r[solver + "_openfoam"] = dict(iters=sorted({o[1] for o in of}), oracle_iters=oit2,
+                                               rel=rel_of, history_ok=bool(hist_ok))
+                ok &= {o[0] for o in of} == {0} and {o[1] for o in of} == {oit2}
+                ok &= rel_of <= 1e-8 and hist_ok
             results[name] = r
     comm.close()
     dist.barrier()
