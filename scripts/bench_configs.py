@@ -185,9 +185,87 @@ def c4(ldu, iters=300):
         dist.destroy_process_group()
 
 
+def c5dist(ldu, n=160, iters=200, slow_rank_sms=None):
+    """NEXT-3 (Eq 5-8): the irregular mesh over N GPUs with (a) equal-cell
+    slabs, (b) nnz-balanced slabs, (c) the paper's measured re-decomposition: per-rank speed
+    s_i = (n_i + 2 o_i) / T_i from each rank's own kernel time T_i with the equal slabs (Eq 5),
+    r_i = s_i / sum s (Eq 6), n_i,new = N r_i (Eq 7-8), re-slab, measure again."""
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uid = [ldu.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = ldu.Comm(rank, world, uid[0], local)
+    g = meshgen.irregular_mesh(n, seed=1505)
+    st = torch.cuda.current_stream()
+    if slow_rank_sms and rank == 0:
+        # emulated heterogeneous node (the paper's Table 2 cluster): rank 0's kernels get only
+        # `slow_rank_sms` SMs (read by ldu_setup when the matrix is configured)
+        os.environ["LDU_RESERVE_SMS"] = str(torch.cuda.get_device_properties(local).multi_processor_count
+                                            - slow_rank_sms)
+    tag = f", rank 0 limited to {slow_rank_sms} SMs" if slow_rank_sms else ""
+
+    def run(bounds, label):
+        part = meshgen.slab_partition(g, world, bounds=bounds)[rank]
+        A = ldu.LduMatrix.from_system(part, comm)
+        A.set_stream(st.cuda_stream)
+        b = torch.from_numpy(part.b).cuda()
+        x = torch.zeros_like(b)
+        A.pipecg_solve(b, x, tol=0.0, maxIter=20)
+        dist.barrier()
+        x.zero_()
+        kms = []
+        for _ in range(2):
+            x.zero_()
+            A.pipecg_solve(b, x, tol=0.0, maxIter=iters, profile=True)
+            stt = A.stats()
+            kms.append((stt["passMs"][1], stt["passLaunches"][1]))
+        if os.environ.get("C5_DEBUG"):
+            print(f"[rank {rank}] {label}: passMs/launches {kms}", flush=True)
+        kern_ms = kms[-1][0]  # this rank's own fused-pass time
+        dist.barrier()
+        torch.cuda.synchronize()
+
+        def solve():
+            x.zero_()
+            return A.pipecg_solve(b, x, tol=0.0, maxIter=iters)
+        t, _ = ev_time(st, solve, 2)
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ks = [None] * world
+        dist.all_gather_object(ks, (kern_ms, part.nCells, part.nFaces))
+        A.close()
+        if rank == 0:
+            km = [k[0] for k in ks]
+            print(json.dumps({"config": f"c5-like irregular {n}^3 base, pipelined CG, {world} GPUs{tag}",
+                              "slabs": label, "iter_per_s": 2 * iters / float(tt.item()),
+                              "rank_kernel_ms": [round(v, 2) for v in km],
+                              "kernel_max_over_min": max(km) / min(km),
+                              "rank_cells": [k[1] for k in ks]}), flush=True)
+        return ks
+
+    ks = run(meshgen.slab_bounds(g.nCells, world), "equal cells")
+    run(meshgen.nnz_balanced_bounds(g, world), "equal non-zeros (static)")
+    # Eq 5-8 from the measured kernel times of the equal-cell run
+    s = [meshgen.speed(nc, nf, kms) for kms, nc, nf in ks]
+    r = meshgen.relative_speeds(s)
+    ks2 = run(meshgen.slab_bounds_weighted(g.nCells, r), "Eq 5-8 measured re-decomposition")
+    # a second application of Eq 5-8 from the re-decomposed run's own times
+    s = [meshgen.speed(nc, nf, kms) for kms, nc, nf in ks2]
+    run(meshgen.slab_bounds_weighted(g.nCells, meshgen.relative_speeds(s)), "Eq 5-8, second pass")
+    comm.close()
+    dist.destroy_process_group()
+
+
 if __name__ == "__main__":
     import paper_1505_07630_b200 as ldu
     which = sys.argv[1] if len(sys.argv) > 1 else "c1"
-    if which != "c4":
+    if which not in ("c4", "c5dist", "c5het"):
         torch.cuda.set_device(0)
-    {"c1": c1, "c2": c2, "c4": c4, "c5": c5}[which](ldu)
+    if which == "c5het":
+        c5dist(ldu, slow_rank_sms=int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+    else:
+        {"c1": c1, "c2": c2, "c4": c4, "c5": c5, "c5dist": c5dist}[which](ldu)
