@@ -4,7 +4,8 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
 ``--impl reference`` leg may import this package.  It wraps ``ldu_oracle.c`` (plain fp64 C,
 ``-O2 -ffp-contract=off``, single thread) through ctypes and shares no code with the CUDA library
 ``paper_1505_07630_b200``.  See ``ldu_oracle.c`` for the passage each function follows and the
-pins that hold it; DESIGN.md lists the readings Z1..Z23 of the paper it relies on.
+pins that hold it; DESIGN.md lists the readings Z1..Z33 of the paper it relies on.
+``oracle.amg`` adds the aggregation-AMG preconditioner of P:236 (NEXT-2; readings Z27-Z33).
 
 Parity status: every function here is pinned by ``tests/test_oracle_*.py`` (no "parity unpinned"
 functions), except that Table 2's absolute iteration counts are unpinned (RHS and stopping

@@ -76,6 +76,10 @@ typedef struct {
     const double *diag, *lower, *upper;
 } ldu_t;
 
+/* Optional preconditioner z = M^-1 r (NULL => Jacobi, z = r / diag).  Used by the AMG
+ * V-cycle below (NEXT-2). */
+typedef struct { void (*apply)(const void *ctx, const double *r, double *z); const void *ctx; } prec_t;
+
 static void amul(const ldu_t *A, const double *x, double *y)
 {
     oracle_amul(A->n, A->nf, A->l, A->u, A->diag, A->lower, A->upper, x, y);
@@ -129,10 +133,10 @@ static int converged(const stop_t *sp, double res, int it)
 
 /* ---- classical Jacobi-PCG (OpenFOAM PCG order) -------------------------- */
 
-int oracle_pcg(int n, int nf, const int *l, const int *u, const double *diag,
-               const double *lower, const double *upper, const double *b, double *x,
-               double tol, int maxIter, int norm, int *nIter, double *finalRes, double *hist,
-               double relTol, int minIter)
+static int pcg_core(int n, int nf, const int *l, const int *u, const double *diag,
+                    const double *lower, const double *upper, const double *b, double *x,
+                    double tol, int maxIter, int norm, int *nIter, double *finalRes, double *hist,
+                    double relTol, int minIter, const prec_t *M)
 {
     if (n <= 0 || nf < 0 || maxIter < 0 || !b || !x || !diag || relTol < 0 || minIter < 0)
         return OR_ERR_ARG;
@@ -163,7 +167,8 @@ int oracle_pcg(int n, int nf, const int *l, const int *u, const double *diag,
 
     double rho_old = 0.0;
     for (int k = 0; k < maxIter; ++k) {
-        for (int c = 0; c < n; ++c) z[c] = rD[c] * r[c];     /* z = M^-1 r */
+        if (M) M->apply(M->ctx, r, z);                        /* z = M^-1 r */
+        else for (int c = 0; c < n; ++c) z[c] = rD[c] * r[c];
         double rho = dot(n, z, r);                            /* rho = (z, r) */
         if (k == 0) {
             for (int c = 0; c < n; ++c) p[c] = z[c];
@@ -191,15 +196,24 @@ out:
     return status;
 }
 
+int oracle_pcg(int n, int nf, const int *l, const int *u, const double *diag,
+               const double *lower, const double *upper, const double *b, double *x,
+               double tol, int maxIter, int norm, int *nIter, double *finalRes, double *hist,
+               double relTol, int minIter)
+{
+    return pcg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, nIter, finalRes,
+                    hist, relTol, minIter, NULL);
+}
+
 /* ---- pipelined CG, Ghysels & Vanroose Alg. 4 with M = diag ------------- */
 
-int oracle_pipecg(int n, int nf, const int *l, const int *u, const double *diag,
-                  const double *lower, const double *upper, const double *b, double *x,
-                  double tol, int maxIter, int norm, int mode, int *nIter, double *finalRes,
-                  double *hist, double relTol, int minIter)
+static int pipecg_core(int n, int nf, const int *l, const int *u, const double *diag,
+                       const double *lower, const double *upper, const double *b, double *x,
+                       double tol, int maxIter, int norm, int mode, int *nIter, double *finalRes,
+                       double *hist, double relTol, int minIter, const prec_t *M)
 {
     if (n <= 0 || nf < 0 || maxIter < 0 || !b || !x || !diag || (mode != 0 && mode != 1) ||
-        relTol < 0 || minIter < 0)
+        relTol < 0 || minIter < 0 || (M && mode != 0))
         return OR_ERR_ARG;
     stop_t sp = {tol, relTol, 0.0, minIter};
     ldu_t A = {n, nf, l, u, diag, lower, upper};
@@ -221,7 +235,8 @@ int oracle_pipecg(int n, int nf, const int *l, const int *u, const double *diag,
         status = OR_OK;
         goto out;
     }
-    for (int c = 0; c < n; ++c) uu[c] = rD[c] * r[c];        /* u = M^-1 r */
+    if (M) M->apply(M->ctx, r, uu);                           /* u = M^-1 r */
+    else for (int c = 0; c < n; ++c) uu[c] = rD[c] * r[c];
     amul(&A, uu, w);                                          /* w = A u */
 
     double gamma_old = 0.0, alpha_old = 0.0;
@@ -238,7 +253,8 @@ int oracle_pipecg(int n, int nf, const int *l, const int *u, const double *diag,
         if (converged(&sp, res, i)) { status = OR_OK; goto out; }
         if (i == maxIter) { status = OR_NOT_CONVERGED; goto out; }
 
-        for (int c = 0; c < n; ++c) m[c] = rD[c] * w[c];      /* m = M^-1 w */
+        if (M) M->apply(M->ctx, w, m);                        /* m = M^-1 w */
+        else for (int c = 0; c < n; ++c) m[c] = rD[c] * w[c];
         amul(&A, m, nn);                                      /* n = A m */
         double alpha, beta;
         if (i == 0) {
@@ -275,4 +291,213 @@ int oracle_pipecg(int n, int nf, const int *l, const int *u, const double *diag,
 out:
     free(r); free(uu); free(w); free(m); free(nn); free(z); free(q); free(s); free(p); free(rD);
     return status;
+}
+
+int oracle_pipecg(int n, int nf, const int *l, const int *u, const double *diag,
+                  const double *lower, const double *upper, const double *b, double *x,
+                  double tol, int maxIter, int norm, int mode, int *nIter, double *finalRes,
+                  double *hist, double relTol, int minIter)
+{
+    return pipecg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, mode, nIter,
+                       finalRes, hist, relTol, minIter, NULL);
+}
+
+/* ==== Aggregation AMG preconditioner (NEXT-2; Table 2) =====================
+ *
+ * The paper preconditions its CG and pipelined CG with CUSP's aggregation AMG: "a V-cycle of an
+ * aggregation-based AMG with weighted Jacobi iterations with omega = 4/3 as a smoother", the
+ * aggregates coming from "the parallel aggregation method based on a distance-2
+ * maximal-independent-set".  Readings Z27-Z33 fix what the paper leaves open:
+ * smoothed aggregation P = (I - w D^-1 A) T with w = (4/3)/rho, rho = max_i sum_j |A_ij| / A_ii;
+ * all couplings strong; one pre- and one post-sweep of w-Jacobi from a zero guess; MIS-2 in the
+ * priority order key(i) below; Galerkin A_c = P^T A P; coarsest level solved exactly (Cholesky).
+ * The hierarchy products are built by oracle/amg.py (scipy); this file holds the integer
+ * aggregation and the V-cycle arithmetic. */
+
+typedef struct { int n; const int *ptr; const int *col; const double *val; } csr_t;
+
+/* y = A x for a CSR matrix, row by row in stored column order. */
+static void csr_mv(const csr_t *A, const double *x, double *y)
+{
+    for (int i = 0; i < A->n; ++i) {
+        double s = 0.0;
+        for (int k = A->ptr[i]; k < A->ptr[i + 1]; ++k) s += A->val[k] * x[A->col[k]];
+        y[i] = s;
+    }
+}
+
+/* Priority key of node i (reading Z30): keyMode 0 = the index itself (lowest index first);
+ * keyMode 1 = (mix32(i) << 32) | i with the "lowbias32" integer mixer, a fixed pseudo-random order
+ * that keeps the parallel MIS rounds few on structured meshes.  Unique by construction. */
+static unsigned long long amg_key(int i, int keyMode)
+{
+    if (keyMode == 0) return (unsigned long long)(unsigned)i;
+    unsigned h = (unsigned)i;
+    h ^= h >> 16; h *= 0x7feb352du; h ^= h >> 15; h *= 0x846ca68bu; h ^= h >> 16;
+    return ((unsigned long long)h << 32) | (unsigned)i;
+}
+
+typedef struct { unsigned long long key; int i; } keyed_t;
+static int cmp_keyed(const void *a, const void *b)
+{
+    unsigned long long x = ((const keyed_t *)a)->key, y = ((const keyed_t *)b)->key;
+    return x < y ? -1 : x > y;
+}
+
+/* Distance-2 MIS aggregation (reading Z30) on the graph of A (off-diagonal entries of the
+ * CSR pattern; values ignored, all couplings strong -- reading Z29).
+ *   1. roots: visit nodes in increasing key; a node becomes a root if no root lies within graph
+ *      distance <= 2 (the greedy = lexicographically-first MIS of the distance-2 graph).
+ *   2. aggregates are numbered by increasing root index.
+ *   3. a non-root adjacent to >= 1 root joins the adjacent root with the smallest key.
+ *   4. every other node (distance exactly 2 from a root) joins the aggregate of its adjacent
+ *      step-3 node with the smallest key.
+ * Writes agg[n]; returns the number of aggregates (or -1 on bad arguments). */
+int oracle_mis2_aggregate(int n, const int *ptr, const int *col, int keyMode, int *agg)
+{
+    if (n <= 0 || !ptr || !col || !agg || (keyMode != 0 && keyMode != 1)) return -1;
+    keyed_t *ord = malloc(sizeof(keyed_t) * (size_t)n);
+    char *root = calloc((size_t)n, 1);
+    for (int i = 0; i < n; ++i) { ord[i].key = amg_key(i, keyMode); ord[i].i = i; }
+    qsort(ord, (size_t)n, sizeof(keyed_t), cmp_keyed);
+    for (int t = 0; t < n; ++t) {                          /* step 1 */
+        int i = ord[t].i, ok = 1;
+        for (int k = ptr[i]; k < ptr[i + 1] && ok; ++k) {
+            int j = col[k];
+            if (j == i) continue;
+            if (root[j]) ok = 0;
+            for (int k2 = ptr[j]; k2 < ptr[j + 1] && ok; ++k2)
+                if (col[k2] != i && root[col[k2]]) ok = 0;
+        }
+        root[i] = (char)ok;
+    }
+    int na = 0;
+    for (int i = 0; i < n; ++i) agg[i] = root[i] ? na++ : -1;   /* step 2 */
+    int *a1 = malloc(sizeof(int) * (size_t)n);
+    for (int i = 0; i < n; ++i) {                          /* step 3 */
+        a1[i] = agg[i];
+        if (root[i]) continue;
+        unsigned long long best = ~0ULL;
+        for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+            int j = col[k];
+            if (j != i && root[j] && amg_key(j, keyMode) < best) { best = amg_key(j, keyMode); a1[i] = agg[j]; }
+        }
+    }
+    for (int i = 0; i < n; ++i) {                          /* step 4 */
+        int a = a1[i];
+        if (a < 0) {
+            unsigned long long best = ~0ULL;
+            for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+                int j = col[k];
+                if (j != i && a1[j] >= 0 && amg_key(j, keyMode) < best) { best = amg_key(j, keyMode); a = a1[j]; }
+            }
+        }
+        agg[i] = a;                                        /* -1 only if isolated from all roots */
+    }
+    free(a1); free(root); free(ord);
+    return na;
+}
+
+/* One AMG hierarchy as handed over by oracle/amg.py.  Level l < L has A_l, P_l (n_l x n_{l+1}),
+ * R_l = P_l^T, rD_l = 1/diag(A_l) and the Jacobi weight w_l; the coarsest matrix (size nc) comes
+ * as its dense lower Cholesky factor Lc (row-major), A_L = Lc Lc^T. */
+typedef struct {
+    int L, nc;
+    const csr_t *A, *P, *R;
+    const double *const *rD;
+    const double *omega;
+    const double *Lc;
+} amg_t;
+
+/* z = A_L^-1 f by forward and back substitution with the Cholesky factor (reading Z31). */
+static void chol_solve(int n, const double *Lc, const double *f, double *z)
+{
+    for (int i = 0; i < n; ++i) {
+        double s = f[i];
+        for (int k = 0; k < i; ++k) s -= Lc[(size_t)i * n + k] * z[k];
+        z[i] = s / Lc[(size_t)i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = z[i];
+        for (int k = i + 1; k < n; ++k) s -= Lc[(size_t)k * n + i] * z[k];
+        z[i] = s / Lc[(size_t)i * n + i];
+    }
+}
+
+/* V-cycle z = B_l f (reading Z32): zero initial guess, one w-Jacobi pre-sweep, residual,
+ * restriction f_c = R r, recursion, prolongation x += P x_c, one w-Jacobi post-sweep. */
+static void vcycle(const amg_t *H, int l, const double *f, double *z)
+{
+    if (l == H->L) { chol_solve(H->nc, H->Lc, f, z); return; }
+    const csr_t *A = &H->A[l];
+    int n = A->n, nc = H->R[l].n;
+    const double w = H->omega[l], *rD = H->rD[l];
+    double *x = calloc((size_t)n, sizeof(double)), *r = calloc((size_t)n, sizeof(double));
+    double *fc = malloc(sizeof(double) * (size_t)nc), *xc = malloc(sizeof(double) * (size_t)nc);
+    double *px = malloc(sizeof(double) * (size_t)n);
+    for (int i = 0; i < n; ++i) x[i] = w * rD[i] * f[i];        /* pre-sweep from x = 0 */
+    csr_mv(A, x, r);
+    for (int i = 0; i < n; ++i) r[i] = f[i] - r[i];             /* r = f - A x */
+    csr_mv(&H->R[l], r, fc);                                    /* f_c = R r */
+    vcycle(H, l + 1, fc, xc);
+    csr_mv(&H->P[l], xc, px);
+    for (int i = 0; i < n; ++i) x[i] += px[i];                  /* x += P x_c */
+    csr_mv(A, x, r);
+    for (int i = 0; i < n; ++i) z[i] = x[i] + w * rD[i] * (f[i] - r[i]);   /* post-sweep */
+    free(x); free(r); free(fc); free(xc); free(px);
+}
+
+static void amg_apply(const void *ctx, const double *r, double *z) { vcycle((const amg_t *)ctx, 0, r, z); }
+
+/* Flat hand-over from Python: per level l < L the CSR arrays of A_l, P_l, R_l, rD_l, omega_l. */
+typedef struct {
+    int L, nc;
+    const int *n;                          /* [L]   rows of A_l                                 */
+    const int *const *Aptr, *const *Acol; const double *const *Aval;
+    const int *const *Pptr, *const *Pcol; const double *const *Pval;
+    const int *const *Rptr, *const *Rcol; const double *const *Rval;
+    const int *nR;                         /* [L]   rows of R_l = n_{l+1}                       */
+    const double *const *rD;
+    const double *omega;
+    const double *Lc;
+} amg_flat_t;
+
+static amg_t amg_unflatten(const amg_flat_t *F, csr_t *buf)
+{
+    csr_t *A = buf, *P = buf + F->L, *R = buf + 2 * F->L;
+    for (int l = 0; l < F->L; ++l) {
+        A[l] = (csr_t){F->n[l], F->Aptr[l], F->Acol[l], F->Aval[l]};
+        P[l] = (csr_t){F->n[l], F->Pptr[l], F->Pcol[l], F->Pval[l]};
+        R[l] = (csr_t){F->nR[l], F->Rptr[l], F->Rcol[l], F->Rval[l]};
+    }
+    amg_t H = {F->L, F->nc, A, P, R, F->rD, F->omega, F->Lc};
+    return H;
+}
+
+/* z = B r, one V-cycle (exported for the preconditioner pins). */
+void oracle_amg_vcycle(const amg_flat_t *F, const double *r, double *z)
+{
+    csr_t *buf = malloc(sizeof(csr_t) * (size_t)(3 * F->L + 1));
+    amg_t H = amg_unflatten(F, buf);
+    vcycle(&H, 0, r, z);
+    free(buf);
+}
+
+/* AMG-preconditioned CG (SURVEY §8(c) c2 with z = B r) and pipelined CG (c3, literal form with
+ * u = B r, m = B w); same criteria and stopping rules as the Jacobi solvers above. */
+int oracle_amg_pcg(int n, int nf, const int *l, const int *u, const double *diag,
+                   const double *lower, const double *upper, const double *b, double *x,
+                   double tol, int maxIter, int norm, int *nIter, double *finalRes, double *hist,
+                   double relTol, int minIter, const amg_flat_t *F, int pipelined)
+{
+    if (!F || F->L < 0 || (F->L > 0 && F->n[0] != n) || (F->L == 0 && F->nc != n)) return OR_ERR_ARG;
+    csr_t *buf = malloc(sizeof(csr_t) * (size_t)(3 * F->L + 1));
+    amg_t H = amg_unflatten(F, buf);
+    prec_t M = {amg_apply, &H};
+    int st = pipelined ? pipecg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, 0,
+                                     nIter, finalRes, hist, relTol, minIter, &M)
+                       : pcg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, nIter,
+                                  finalRes, hist, relTol, minIter, &M);
+    free(buf);
+    return st;
 }
