@@ -198,6 +198,69 @@ ldu_status ldu_get_info(ldu_handle h, ldu_info *out);
  * Roofline denominator cross-check.  Uses its own scratch allocation. */
 ldu_status ldu_stream_triad(int device, long long n, int reps, double *gbps);
 
+/* ---- aggregation-AMG preconditioner ------------------------------------
+ * "a V-cycle of an aggregation-based AMG with weighted Jacobi iterations with omega = 4/3
+ * as a smoother ... the parallel aggregation method based on a distance-2
+ * maximal-independent-set"; Table 2 runs it inside CG ("GPU AMG-CG") and pipelined
+ * CG ("GPU AMG-PipeCG").  Readings Z27-Z34:
+ *   - aggregates: greedy distance-2 MIS in the priority order of keyMode (Z30), all couplings
+ *     strong (Z29); a DIA-layout coefficient that is exactly 0 is not a coupling (Z34);
+ *   - prolongator: smoothed aggregation P = (I - w D^-1 A) T, w = (4/3) / (1.05 x the largest
+ *     Ritz value of 20 Lanczos steps on D^-1/2 A D^-1/2) (Z27); R = P^T; A_c = P^T A P (Z32);
+ *   - smoother: one pre- and one post-sweep of w-Jacobi from x = 0 (Z28);
+ *   - coarsening while n > coarsest, the level shrinks and fewer than maxLevels levels exist; the
+ *     coarsest system is solved exactly through its dense inverse (Z31; at most 8192 rows);
+ *   - multi-rank handles: the hierarchy is built from the rank's local matrix (interfaces
+ *     dropped, block-Jacobi across ranks; Z33).  Not supported yet: returns LDU_ERR_STATE.
+ * The matrix must be symmetric (lower == NULL or lower == upper); diag > 0.                     */
+typedef struct {
+  int coarsest;        /* stop coarsening at n <= coarsest; 0 = 64 (reading Z31)                 */
+  int maxLevels;       /* at most this many coarsening steps; 0 = 25                             */
+  int keyIndexOrder;   /* MIS-2 priority: 0 = hashed key (mix32(i) << 32 | i, default), 1 = index */
+  int unsmoothed;      /* 0 = smoothed aggregation (default), 1 = piecewise-constant P = T       */
+  int lanczosSteps;    /* Lanczos steps of the rho(D^-1 A) estimate; 0 = 20                      */
+  int reserved[3];     /* must be zero                                                           */
+} ldu_amg_opts;
+
+#define LDU_AMG_MAX_LEVELS 25
+
+typedef struct {
+  int nLevels;                                  /* L = number of coarsening steps (0: direct)   */
+  int coarsestN;                                /* rows of the coarsest matrix A_L              */
+  int n[LDU_AMG_MAX_LEVELS + 1];                /* rows of A_0 .. A_L                            */
+  long long nnzA[LDU_AMG_MAX_LEVELS + 1];       /* stored entries of A_0 .. A_L (diag included) */
+  long long nnzP[LDU_AMG_MAX_LEVELS];           /* stored entries of P_0 .. P_{L-1} (= of R_l)  */
+  double omega[LDU_AMG_MAX_LEVELS];             /* Jacobi weights w_0 .. w_{L-1}                 */
+  double operatorComplexity;                    /* sum_l nnz(A_l) / nnz(A_0)                     */
+  double setupMs;                               /* device time of ldu_amg_setup                  */
+  long long deviceBytes;                        /* device memory held by the hierarchy           */
+} ldu_amg_info;
+
+/* Builds the hierarchy on the device for handle h (replacing any previous one).  opts NULL =>
+ * defaults.  Errors: INVALID_ARG (bad option, non-symmetric matrix, coarsest level > 8192 rows),
+ * STATE (multi-rank handle; a non-positive pivot in the coarsest inverse), CUDA, OOM. */
+ldu_status ldu_amg_setup(ldu_handle h, const ldu_amg_opts *opts);
+ldu_status ldu_amg_get_info(ldu_handle h, ldu_amg_info *out);
+
+/* Host copies of level `level` of the hierarchy (for verification).  which = 0: A_level
+ * (level in [0, L]); 1: P_level; 2: R_level (level in [0, L)).  ptr [rows + 1], col / val [nnz]
+ * (sizes from ldu_amg_get_info; R_l has n[l+1] rows and nnzP[l] entries); any of them may be NULL.
+ * ldu_amg_get_aggregates: agg [n[level]] (level in [0, L)).  STATE if no hierarchy. */
+ldu_status ldu_amg_get_matrix(ldu_handle h, int level, int which, int *ptr, int *col, double *val);
+ldu_status ldu_amg_get_aggregates(ldu_handle h, int level, int *agg);
+
+/* z = B r: one V-cycle of the hierarchy (reading Z32).  r, z: [nCells] host or device. */
+ldu_status ldu_amg_vcycle(ldu_handle h, const double *r, double *z);
+
+/* AMG-preconditioned classical CG (SURVEY §8(c) c2 with z = B r; 2 reductions per iteration
+ * plus the V-cycle) and pipelined CG (c3 literal Ghysels-Vanroose form with u = B r, m = B w; one
+ * fused reduction per iteration).  Same arguments, options and semantics as pcg_solve_ex;
+ * STATE if ldu_amg_setup has not been called. */
+ldu_status amg_pcg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,
+                         const ldu_solve_opts *opts, int *nIter, double *finalRes);
+ldu_status amg_pipecg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,
+                            const ldu_solve_opts *opts, int *nIter, double *finalRes);
+
 ldu_status ldu_destroy(ldu_handle h);
 const char *ldu_last_error(void);
 int ldu_abi_version(void);

@@ -158,6 +158,28 @@ class Hierarchy:
         return sum(nnz) / nnz[0]
 
 
+def prolongator(A: sp.csr_matrix, agg: np.ndarray, nAgg: int, w: float,
+                smooth: bool = True) -> sp.csr_matrix:
+    """P = (I - w D^-1 A) T (smoothed aggregation, reading Z27) or P = T; T[i, agg[i]] = 1."""
+    n = A.shape[0]
+    T = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, nAgg))
+    if smooth:
+        P = (T - sp.diags(w / A.diagonal()) @ (A @ T)).tocsr()
+    else:
+        P = T
+    P.sort_indices()
+    return P
+
+
+def galerkin(A: sp.csr_matrix, P: sp.csr_matrix):
+    """R = P^T and the Galerkin coarse matrix A_c = R A P (reading Z32)."""
+    R = P.T.tocsr()
+    R.sort_indices()
+    Ac = (R @ A @ P).tocsr()
+    Ac.sort_indices()
+    return R, Ac
+
+
 def build_hierarchy(A, coarsest: int = 64, max_levels: int = 25, key_mode: int = KEY_HASH,
                     smooth: bool = True, max_dense: int = 8192, factor: bool = True) -> Hierarchy:
     """Smoothed-aggregation hierarchy (readings Z27-Z32).  ``A`` is an LDU system or a CSR."""
@@ -171,17 +193,9 @@ def build_hierarchy(A, coarsest: int = 64, max_levels: int = 25, key_mode: int =
         agg, na = mis2_aggregate(A, key_mode)
         if na >= n:                                   # no coarsening possible (Z31)
             break
-        T = sp.csr_matrix((np.ones(n), (np.arange(n), agg)), shape=(n, na))
         w = jacobi_weight(A)
-        if smooth:                                    # P = (I - w D^-1 A) T  (Z27)
-            P = (T - sp.diags(w / A.diagonal()) @ (A @ T)).tocsr()
-        else:
-            P = T
-        P.sort_indices()
-        R = P.T.tocsr()
-        R.sort_indices()
-        Ac = (R @ A @ P).tocsr()                      # Galerkin (Z32)
-        Ac.sort_indices()
+        P = prolongator(A, agg, na, w, smooth)
+        R, Ac = galerkin(A, P)
         levels.append(Level(A, agg, na, w, P, R))
         A = Ac
     if A.shape[0] > max_dense:

@@ -86,6 +86,32 @@ class Info(ctypes.Structure):
         return d
 
 
+AMG_MAX_LEVELS = 25
+
+
+class AmgOpts(ctypes.Structure):
+    _fields_ = [("coarsest", ctypes.c_int), ("maxLevels", ctypes.c_int),
+                ("keyIndexOrder", ctypes.c_int), ("unsmoothed", ctypes.c_int),
+                ("lanczosSteps", ctypes.c_int), ("reserved", ctypes.c_int * 3)]
+
+
+class AmgInfo(ctypes.Structure):
+    _fields_ = [("nLevels", ctypes.c_int), ("coarsestN", ctypes.c_int),
+                ("n", ctypes.c_int * (AMG_MAX_LEVELS + 1)),
+                ("nnzA", ctypes.c_longlong * (AMG_MAX_LEVELS + 1)),
+                ("nnzP", ctypes.c_longlong * AMG_MAX_LEVELS),
+                ("omega", ctypes.c_double * AMG_MAX_LEVELS),
+                ("operatorComplexity", ctypes.c_double), ("setupMs", ctypes.c_double),
+                ("deviceBytes", ctypes.c_longlong)]
+
+    def as_dict(self):
+        L = self.nLevels
+        return {"nLevels": L, "coarsestN": self.coarsestN, "n": list(self.n)[: L + 1],
+                "nnzA": list(self.nnzA)[: L + 1], "nnzP": list(self.nnzP)[:L],
+                "omega": list(self.omega)[:L], "operatorComplexity": self.operatorComplexity,
+                "setupMs": self.setupMs, "deviceBytes": self.deviceBytes}
+
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _D = ctypes.c_double
@@ -111,6 +137,15 @@ SIGNATURES = {
     "ldu_get_solve_stats": (_S, [_P, ctypes.POINTER(SolveStats)]),
     "ldu_get_info": (_S, [_P, ctypes.POINTER(Info)]),
     "ldu_stream_triad": (_S, [_I, ctypes.c_longlong, _I, ctypes.POINTER(_D)]),
+    "ldu_amg_setup": (_S, [_P, ctypes.POINTER(AmgOpts)]),
+    "ldu_amg_get_info": (_S, [_P, ctypes.POINTER(AmgInfo)]),
+    "ldu_amg_get_matrix": (_S, [_P, _I, _I, _P, _P, _P]),
+    "ldu_amg_get_aggregates": (_S, [_P, _I, _P]),
+    "ldu_amg_vcycle": (_S, [_P, _P, _P]),
+    "amg_pcg_solve": (_S, [_P, _P, _P, _D, _I, ctypes.POINTER(SolveOpts), ctypes.POINTER(_I),
+                           ctypes.POINTER(_D)]),
+    "amg_pipecg_solve": (_S, [_P, _P, _P, _D, _I, ctypes.POINTER(SolveOpts), ctypes.POINTER(_I),
+                              ctypes.POINTER(_D)]),
     "ldu_destroy": (_S, [_P]),
 }
 for _name, (_res, _args) in SIGNATURES.items():
@@ -242,6 +277,62 @@ class LduMatrix:
         """Ghysels-Vanroose pipelined CG; x is in/out.  Returns (status, nIter, finalRes)."""
         return self._solve(_lib.pipecg_solve_ex, b, x, tol, maxIter, norm, record_history, batch,
                            profile, relTol, minIter)
+
+    # -- aggregation-AMG preconditioner (NEXT-2, P:236) --------------------------------------
+    def amg_setup(self, coarsest: int = 0, maxLevels: int = 0, keyIndexOrder: bool = False,
+                  unsmoothed: bool = False, lanczosSteps: int = 0) -> dict:
+        """Build the smoothed-aggregation hierarchy on the device; returns amg_info()."""
+        o = AmgOpts(int(coarsest), int(maxLevels), 1 if keyIndexOrder else 0,
+                    1 if unsmoothed else 0, int(lanczosSteps))
+        _check(_lib.ldu_amg_setup(self.handle, ctypes.byref(o)))
+        return self.amg_info()
+
+    def amg_info(self) -> dict:
+        i = AmgInfo()
+        _check(_lib.ldu_amg_get_info(self.handle, ctypes.byref(i)))
+        return i.as_dict()
+
+    def amg_matrix(self, level: int, which: str = "A"):
+        """(indptr, indices, data) numpy arrays of A_level / P_level / R_level (host copies)."""
+        import numpy as np
+        info = self.amg_info()
+        w = {"A": 0, "P": 1, "R": 2}[which]
+        if w == 0:
+            rows, nnz = info["n"][level], info["nnzA"][level]
+        else:
+            rows = info["n"][level] if w == 1 else info["n"][level + 1]
+            nnz = info["nnzP"][level]
+        ptr = np.empty(rows + 1, dtype=np.int32)
+        col = np.empty(max(1, nnz), dtype=np.int32)
+        val = np.empty(max(1, nnz), dtype=np.float64)
+        _check(_lib.ldu_amg_get_matrix(self.handle, int(level), w, ptr.ctypes.data,
+                                       col.ctypes.data, val.ctypes.data))
+        return ptr, col[:nnz], val[:nnz]
+
+    def amg_aggregates(self, level: int):
+        import numpy as np
+        agg = np.empty(self.amg_info()["n"][level], dtype=np.int32)
+        _check(_lib.ldu_amg_get_aggregates(self.handle, int(level), agg.ctypes.data))
+        return agg
+
+    def amg_vcycle(self, r, z):
+        """z = B r (one V-cycle)."""
+        _check(_lib.ldu_amg_vcycle(self.handle, _ptr(r, "f64"), _ptr(z, "f64")))
+        return z
+
+    def amg_pcg_solve(self, b, x, tol: float = 1e-10, maxIter: int = 10000, norm: int = NORM_L2,
+                      record_history: bool = False, batch: int = 0, profile: bool = False,
+                      relTol: float = 0.0, minIter: int = 0):
+        """AMG-preconditioned CG; x is in/out.  Returns (status, nIter, finalRes)."""
+        return self._solve(_lib.amg_pcg_solve, b, x, tol, maxIter, norm, record_history, batch,
+                           profile, relTol, minIter)
+
+    def amg_pipecg_solve(self, b, x, tol: float = 1e-10, maxIter: int = 10000,
+                         norm: int = NORM_L2, record_history: bool = False, batch: int = 0,
+                         profile: bool = False, relTol: float = 0.0, minIter: int = 0):
+        """AMG-preconditioned pipelined CG (literal GV form); x is in/out."""
+        return self._solve(_lib.amg_pipecg_solve, b, x, tol, maxIter, norm, record_history,
+                           batch, profile, relTol, minIter)
 
     def history(self):
         import numpy as np

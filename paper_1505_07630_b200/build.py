@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libldu_b200.so")
-SRCS = [os.path.join(HERE, "csrc", f) for f in ("ldu_setup.cu", "ldu_solve.cu", "ldu_api.cu")]
+SRCS = [os.path.join(HERE, "csrc", f) for f in ("ldu_setup.cu", "ldu_solve.cu", "ldu_amg_setup.cu", "ldu_api.cu")]
 DEPS = SRCS + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "ldu.h")]
 
 

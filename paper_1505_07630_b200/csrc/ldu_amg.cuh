@@ -1,0 +1,110 @@
+// ldu_amg.cuh -- aggregation-AMG preconditioner of libldu_b200 (NEXT-2; Table 2).
+//
+// The paper preconditions CG and pipelined CG with "a V-cycle of an aggregation-based AMG with
+// weighted Jacobi iterations with omega = 4/3 as a smoother", the aggregates coming from "the
+// parallel aggregation method based on a distance-2 maximal-independent-set".  Readings
+// Z27-Z34 fix the rest.  Everything is built and applied on the device:
+//   setup (ldu_amg_setup.cu): level-0 CSR from the handle's layout, MIS-2 aggregation by parallel
+//     local-minimum rounds, Lanczos estimate of rho(D^-1 A), smoothed prolongator
+//     P = (I - w D^-1 A) T, R = P^T and the Galerkin product A_c = P^T (A P) by sort-based
+//     sparse products (expand -> CUB radix sort -> fixed-order segment sums), coarsest level
+//     inverted densely (Gauss-Jordan);
+//   solve (ldu_amg_solve.cuh, included by ldu_solve.cu): V-cycle kernels (level 0 in the handle's
+//     DIA / SELL layout, coarser levels CSR with a sub-warp per row), AMG-PCG and AMG-PipeCG.
+#pragma once
+
+#include <vector>
+
+#include "ldu_impl.cuh"
+
+namespace ldu {
+
+// CSR matrix in device memory, ascending columns per row, diagonal stored.
+struct CsrMat {
+  int nrows = 0, ncols = 0;
+  long long nnz = 0;
+  int* ptr = nullptr;     // [nrows + 1]
+  int* col = nullptr;     // [nnz]
+  double* val = nullptr;  // [nnz]
+  int group = 1;          // lanes per row of the CSR-vector SpMV (power of two <= 32)
+  void release() {
+    dfree(ptr);
+    dfree(col);
+    dfree(val);
+    ptr = nullptr;
+    col = nullptr;
+    val = nullptr;
+    nnz = 0;
+  }
+};
+
+// Device view of a CsrMat.
+struct CsrView {
+  int n;
+  const int* __restrict__ ptr;
+  const int* __restrict__ col;
+  const double* __restrict__ val;
+};
+
+inline CsrView view(const CsrMat& m) { return CsrView{m.nrows, m.ptr, m.col, m.val}; }
+
+// One level l < L of the hierarchy: A_l (n x n), aggregates, P_l (n x nc), R_l = P_l^T.
+struct AmgLevel {
+  int n = 0, nc = 0;
+  CsrMat A;                  // A_l (level 0: CSR copy of the handle's matrix; setup / export)
+  double* diag = nullptr;    // level 0: the handle's arrays (not owned)
+  double* rD = nullptr;
+  double omega = 0.0;        // Jacobi weight (4/3) / rho (reading Z27)
+  int* agg = nullptr;        // [n] aggregate of each row
+  CsrMat P, R;
+  double* r = nullptr;       // V-cycle work: residual after the pre-sweep
+  double* x = nullptr;       //               iterate after the prolongation
+  double* f = nullptr;       // right-hand side (level >= 1)
+  double* z = nullptr;       // V-cycle result (level >= 1)
+  bool ownsDiag = false;
+};
+
+struct AmgHierarchy {
+  ldu_amg_opts opts{};
+  std::vector<AmgLevel> lv;  // levels 0 .. L-1
+  int L = 0;
+  int nc = 0;                // coarsest size (level L)
+  CsrMat Ac;                 // coarsest matrix (export; level L == 0 => copy of A_0)
+  double* Ainv = nullptr;    // [nc * nc] row-major inverse of the coarsest matrix (reading Z31)
+  double* fL = nullptr;      // coarsest right-hand side / result (level L >= 1)
+  double* zL = nullptr;
+  double setupMs = 0.0;
+  // AMG Krylov work vectors (lazily allocated by the solves)
+  double *u = nullptr, *m = nullptr, *zk = nullptr, *qk = nullptr;
+  // iteration-batch graphs: [pipelined + 2 * profile]
+  cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
+  int graphBatch[4] = {0, 0, 0, 0};
+  long long graphKernels[4] = {0, 0, 0, 0};
+};
+
+void amg_setup(ldu_handle h, const ldu_amg_opts* opts);
+void amg_release(ldu_handle h);
+void amg_info(ldu_handle h, ldu_amg_info* out);
+void amg_export(ldu_handle h, int level, int which, int* ptr, int* col, double* val);
+void amg_export_agg(ldu_handle h, int level, int* agg);
+// ldu_solve.cu
+void amg_vcycle(ldu_handle h, const double* r, double* z);
+ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, double tol,
+                     int maxIter, const ldu_solve_opts* opts, int* nIter, double* finalRes);
+
+// Priority key of node i in the MIS-2 rounds (reading Z30): keyMode 0 = index, 1 = the
+// "lowbias32" mixer in the high word and the index in the low word (unique).
+__host__ __device__ __forceinline__ unsigned amg_mix32(unsigned h) {
+  h ^= h >> 16;
+  h *= 0x7feb352du;
+  h ^= h >> 15;
+  h *= 0x846ca68bu;
+  h ^= h >> 16;
+  return h;
+}
+__host__ __device__ __forceinline__ unsigned long long amg_key(int i, int hashed) {
+  return hashed ? (((unsigned long long)amg_mix32((unsigned)i) << 32) | (unsigned)i)
+                : (unsigned long long)(unsigned)i;
+}
+
+}  // namespace ldu

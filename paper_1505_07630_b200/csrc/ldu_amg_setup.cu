@@ -1,0 +1,1044 @@
+// ldu_amg_setup.cu -- device-side setup of the aggregation-AMG hierarchy (NEXT-2).
+//
+// Per level l (readings Z27-Z32):
+//   1. graph of A_l = its off-diagonal pattern (all couplings strong, Z29);
+//   2. distance-2 MIS by parallel local-minimum rounds in key order: a node becomes a root when
+//      its key is the smallest among the undecided nodes within distance 2; the roots and all
+//      nodes within distance 2 of them are then decided.  This is exactly the greedy
+//      (lexicographically first) MIS-2 in key order (Z30); aggregates are numbered by root index,
+//      a node next to roots joins the smallest-key adjacent root, the rest join the aggregate of
+//      their smallest-key adjacent step-3 node;
+//   3. w_l = (4/3) / (1.05 x largest Ritz value of `lanczosSteps` Lanczos steps on
+//      D^-1/2 A D^-1/2 from v0_i = mix32(i)/2^32 - 1/2) (Z27);
+//   4. P = T - diag(w / a_ii) (A T) (smoothed aggregation, Z27), R = P^T, A_{l+1} = P^T (A P)
+//      (Galerkin, Z32) -- each sparse product is expanded into (row, col, value) triples in a
+//      fixed order, radix-sorted by (row, col) (stable), and equal keys are summed sequentially in
+//      expansion order: deterministic, no floating-point atomics.  Exact zeros produced by the
+//      products are dropped (as a sparse product does);
+//   5. the coarsest matrix is inverted densely by Gauss-Jordan elimination (SPD: no pivoting).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "ldu_amg.cuh"
+#include "ldu_kernels.cuh"
+
+namespace ldu {
+
+namespace {
+
+constexpr int kSB = 256;
+constexpr unsigned long long kInfKey = ~0ULL;
+
+int nblk(long long n) {
+  long long b = (n + kSB - 1) / kSB;
+  return (int)std::max(1LL, std::min(b, 148LL * 64));
+}
+
+#define GSTRIDE(i, n)                                                                 \
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)(n); \
+       i += (long long)gridDim.x * blockDim.x)
+
+struct Scratch {  // frees every registered allocation on scope exit
+  std::vector<void*> p;
+  template <class T>
+  T* get(size_t n) {
+    T* q = dmalloc<T>(n);
+    p.push_back(q);
+    return q;
+  }
+  ~Scratch() {
+    for (void* q : p) dfree(q);
+  }
+};
+
+template <class T>
+T d2h(const T* d, cudaStream_t s) {
+  T v;
+  CUDA_CHECK(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  return v;
+}
+
+// exclusive scan of in[0..n) into out[0..n] (out[n] = total)
+template <class T>
+void exclusive_scan(const T* in, T* out, long long n, cudaStream_t s) {
+  Scratch sc;
+  T* tmp = sc.get<T>(n + 1);
+  CUDA_CHECK(cudaMemsetAsync(tmp + n, 0, sizeof(T), s));
+  if (n) CUDA_CHECK(cudaMemcpyAsync(tmp, in, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  size_t bytes = 0;
+  CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, tmp, out, n + 1, s));
+  void* ws = sc.get<char>(bytes);
+  CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws, bytes, tmp, out, n + 1, s));
+}
+
+int group_of(long long nnz, int rows) {
+  const double avg = rows ? (double)nnz / rows : 1.0;
+  int g = 1;
+  while (g < 32 && g < avg) g <<= 1;
+  return g;
+}
+
+// ---------------------------------------------------------------------------------------------
+// sparse assembly: triples (key = row * ncols + col, value) -> CSR, duplicates summed in order
+// ---------------------------------------------------------------------------------------------
+__global__ void k_seg_sum(long long m, const unsigned long long* __restrict__ key,
+                          double* __restrict__ val, long long* __restrict__ keep, int drop) {
+  GSTRIDE(k, m) {
+    const unsigned long long kk = key[k];
+    const bool head = (k == 0) || key[k - 1] != kk;
+    long long flag = 0;
+    if (head) {
+      double s = val[k];
+      for (long long t = k + 1; t < m && key[t] == kk; ++t) s += val[t];
+      val[k] = s;  // only this thread touches slots [k, next head)
+      flag = (!drop || s != 0.0) ? 1 : 0;
+    }
+    keep[k] = flag;
+  }
+}
+
+__global__ void k_emit(long long m, int ncols, const unsigned long long* __restrict__ key,
+                       const double* __restrict__ val, const long long* __restrict__ keep,
+                       const long long* __restrict__ pos, int* __restrict__ col,
+                       double* __restrict__ out, int* __restrict__ rowcnt) {
+  GSTRIDE(k, m) {
+    if (!keep[k]) continue;
+    const unsigned long long kk = key[k];
+    const long long p = pos[k];
+    col[p] = (int)(kk % (unsigned long long)ncols);
+    out[p] = val[k];
+    atomicAdd(rowcnt + (kk / (unsigned long long)ncols), 1);  // integer: order-independent
+  }
+}
+
+int bits_for(unsigned long long v) {
+  int b = 1;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+// keys / vals [m] are consumed (clobbered).
+CsrMat assemble(int nrows, int ncols, long long m, unsigned long long* keys, double* vals,
+                bool drop, cudaStream_t s) {
+  Scratch sc;
+  CsrMat out;
+  out.nrows = nrows;
+  out.ncols = ncols;
+  unsigned long long* k2 = sc.get<unsigned long long>(m);
+  double* v2 = sc.get<double>(m);
+  const int endbit = bits_for((unsigned long long)nrows * (unsigned long long)ncols);
+  if (m > 0) {
+    size_t bytes = 0;
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, k2, vals, v2, m, 0, endbit, s));
+    void* ws = sc.get<char>(bytes);
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ws, bytes, keys, k2, vals, v2, m, 0, endbit, s));
+  }
+  long long* keep = sc.get<long long>(m + 1);
+  long long* pos = sc.get<long long>(m + 1);
+  if (m > 0) k_seg_sum<<<nblk(m), kSB, 0, s>>>(m, k2, v2, keep, drop ? 1 : 0);
+  exclusive_scan<long long>(keep, pos, m, s);
+  const long long nnz = d2h(pos + m, s);
+  if (nnz >= (1LL << 31) - 1) throw Error(LDU_ERR_OOM, "AMG level exceeds 2^31 stored entries");
+  out.nnz = nnz;
+  out.col = dmalloc<int>(nnz);
+  out.val = dmalloc<double>(nnz);
+  int* rowcnt = sc.get<int>(nrows + 1);
+  CUDA_CHECK(cudaMemsetAsync(rowcnt, 0, sizeof(int) * (nrows + 1), s));
+  if (m > 0) k_emit<<<nblk(m), kSB, 0, s>>>(m, ncols, k2, v2, keep, pos, out.col, out.val, rowcnt);
+  out.ptr = dmalloc<int>(nrows + 1);
+  exclusive_scan<int>(rowcnt, out.ptr, nrows, s);
+  CUDA_CHECK(cudaGetLastError());
+  out.group = group_of(out.nnz, nrows);
+  return out;
+}
+
+// ---------------------------------------------------------------------------------------------
+// level 0: CSR (diag included) from the handle's layout
+// ---------------------------------------------------------------------------------------------
+// f(j, a) for the off-diagonal entries of row c in ascending column order.  DIA: a coefficient
+// that is exactly 0 is not a coupling (reading Z34: the layout stores 0 where there is no face).
+template <int ND, class F>
+__device__ __forceinline__ void for_row(const DiaView<ND>& A, int c, F f) {
+#pragma unroll
+  for (int k = ND - 1; k >= 0; --k) {
+    const int j = c - A.off[k];
+    if (j >= 0) {
+      const double a = A.U[k][j];
+      if (a != 0.0) f(j, a);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < ND; ++k) {
+    const int j = c + A.off[k];
+    if (j < A.n) {
+      const double a = A.U[k][c];
+      if (a != 0.0) f(j, a);
+    }
+  }
+}
+
+template <class F>
+__device__ __forceinline__ void for_row(const SellView& A, int c, F f) {
+  const int slice = c >> 5, lane = c & 31;
+  const long long base = A.slicePtr[slice];
+  const int np = A.npairs[slice];
+  for (int jj = 0; jj < np; ++jj) {
+    const long long e = (base + jj) * 32 + lane;
+    const int2 cc = A.col[e];
+    const double2 vv = A.val[e];
+    if (cc.x < 0) break;
+    f(cc.x, vv.x);
+    if (cc.y < 0) break;
+    f(cc.y, vv.y);
+  }
+}
+
+template <class Fmt>
+__global__ void k_l0_count(Fmt A, long long* __restrict__ cnt) {
+  GSTRIDE(c, A.n) {
+    long long k = 1;
+    for_row(A, (int)c, [&](int, double) { ++k; });
+    cnt[c] = k;
+  }
+}
+
+template <class Fmt>
+__global__ void k_l0_fill(Fmt A, const double* __restrict__ diag, const long long* __restrict__ off,
+                          unsigned long long* __restrict__ key, double* __restrict__ val) {
+  GSTRIDE(c, A.n) {
+    long long o = off[c];
+    const unsigned long long rowk = (unsigned long long)c * (unsigned long long)A.n;
+    bool diagDone = false;
+    for_row(A, (int)c, [&](int j, double a) {
+      if (!diagDone && j > c) {
+        key[o] = rowk + c;
+        val[o++] = diag[c];
+        diagDone = true;
+      }
+      key[o] = rowk + j;
+      val[o++] = a;
+    });
+    if (!diagDone) {
+      key[o] = rowk + c;
+      val[o] = diag[c];
+    }
+  }
+}
+
+template <class F>
+void with_layout(ldu_handle h, F&& f) {
+  if (h->layout == LDU_LAYOUT_SELL32) {
+    f(SellView{h->n, h->slicePtr, h->npairs, h->col, h->val});
+    return;
+  }
+  auto dia = [&](auto tag) {
+    constexpr int ND = decltype(tag)::value;
+    DiaView<ND> v;
+    v.n = h->n;
+    for (int k = 0; k < ND; ++k) {
+      v.off[k] = h->off[k];
+      v.U[k] = h->U + (size_t)k * h->n;
+    }
+    f(v);
+  };
+  switch (h->nd) {
+    case 1: dia(std::integral_constant<int, 1>()); break;
+    case 2: dia(std::integral_constant<int, 2>()); break;
+    case 3: dia(std::integral_constant<int, 3>()); break;
+    case 4: dia(std::integral_constant<int, 4>()); break;
+    case 5: dia(std::integral_constant<int, 5>()); break;
+    case 6: dia(std::integral_constant<int, 6>()); break;
+    case 7: dia(std::integral_constant<int, 7>()); break;
+    case 8: dia(std::integral_constant<int, 8>()); break;
+    default: throw Error(LDU_ERR_STATE, "bad DIA offset count");
+  }
+}
+
+CsrMat level0_csr(ldu_handle h, cudaStream_t s) {
+  Scratch sc;
+  const int n = h->n;
+  long long* cnt = sc.get<long long>(n + 1);
+  long long* off = sc.get<long long>(n + 1);
+  with_layout(h, [&](auto A) { k_l0_count<<<nblk(n), kSB, 0, s>>>(A, cnt); });
+  exclusive_scan<long long>(cnt, off, n, s);
+  const long long m = d2h(off + n, s);
+  unsigned long long* key = sc.get<unsigned long long>(m);
+  double* val = sc.get<double>(m);
+  with_layout(h, [&](auto A) { k_l0_fill<<<nblk(n), kSB, 0, s>>>(A, h->diag, off, key, val); });
+  CUDA_CHECK(cudaGetLastError());
+  return assemble(n, n, m, key, val, false, s);
+}
+
+// ---------------------------------------------------------------------------------------------
+// distance-2 MIS aggregation (reading Z30)
+// ---------------------------------------------------------------------------------------------
+__global__ void k_mis_min1(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                           const unsigned char* __restrict__ und, int hashed,
+                           unsigned long long* __restrict__ m1) {
+  GSTRIDE(i, n) {
+    unsigned long long m = und[i] ? amg_key((int)i, hashed) : kInfKey;
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+      const int j = col[k];
+      if (j != i && und[j]) m = min(m, amg_key(j, hashed));
+    }
+    m1[i] = m;
+  }
+}
+
+__global__ void k_mis_min2(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                           const unsigned char* __restrict__ und, int hashed,
+                           const unsigned long long* __restrict__ m1,
+                           unsigned char* __restrict__ fresh, unsigned char* __restrict__ root) {
+  GSTRIDE(i, n) {
+    unsigned long long m = m1[i];
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) m = min(m, m1[col[k]]);
+    const bool nr = und[i] && m == amg_key((int)i, hashed);
+    fresh[i] = nr ? 1 : 0;
+    if (nr) root[i] = 1;
+  }
+}
+
+// d[i] = src[i] or any src[j] over the neighbours
+__global__ void k_mis_spread(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                             const unsigned char* __restrict__ src, unsigned char* __restrict__ d) {
+  GSTRIDE(i, n) {
+    unsigned char v = src[i];
+    for (int k = ptr[i]; k < ptr[i + 1] && !v; ++k) v = src[col[k]];
+    d[i] = v;
+  }
+}
+
+__global__ void k_mis_retire(int n, const unsigned char* __restrict__ d2,
+                             unsigned char* __restrict__ und, int* __restrict__ left) {
+  int cnt = 0;
+  GSTRIDE(i, n) {
+    if (und[i] && d2[i]) und[i] = 0;
+    cnt += und[i];
+  }
+  if (cnt) atomicAdd(left, cnt);
+}
+
+__global__ void k_root_flags(int n, const unsigned char* __restrict__ root, int* __restrict__ f) {
+  GSTRIDE(i, n) f[i] = root[i];
+}
+
+// step 3: a1[i] = own aggregate (root) or that of the smallest-key adjacent root, else -1
+__global__ void k_agg_step3(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                            const unsigned char* __restrict__ root, const int* __restrict__ rootIdx,
+                            int hashed, int* __restrict__ a1) {
+  GSTRIDE(i, n) {
+    int a = -1;
+    if (root[i]) {
+      a = rootIdx[i];
+    } else {
+      unsigned long long best = kInfKey;
+      for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+        const int j = col[k];
+        if (j != i && root[j]) {
+          const unsigned long long kj = amg_key(j, hashed);
+          if (kj < best) {
+            best = kj;
+            a = rootIdx[j];
+          }
+        }
+      }
+    }
+    a1[i] = a;
+  }
+}
+
+// step 4: the rest join the aggregate of their smallest-key adjacent step-3 node
+__global__ void k_agg_step4(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                            const int* __restrict__ a1, int hashed, int* __restrict__ agg,
+                            int* __restrict__ orphan) {
+  GSTRIDE(i, n) {
+    int a = a1[i];
+    if (a < 0) {
+      unsigned long long best = kInfKey;
+      for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+        const int j = col[k];
+        if (j != i && a1[j] >= 0) {
+          const unsigned long long kj = amg_key(j, hashed);
+          if (kj < best) {
+            best = kj;
+            a = a1[j];
+          }
+        }
+      }
+    }
+    agg[i] = a;
+    if (a < 0) atomicAdd(orphan, 1);
+  }
+}
+
+int mis2_aggregate(const CsrMat& A, int hashed, int* agg, cudaStream_t s) {
+  Scratch sc;
+  const int n = A.nrows;
+  unsigned char* und = sc.get<unsigned char>(n);
+  unsigned char* root = sc.get<unsigned char>(n);
+  unsigned char* fresh = sc.get<unsigned char>(n);
+  unsigned char* d1 = sc.get<unsigned char>(n);
+  unsigned char* d2 = sc.get<unsigned char>(n);
+  unsigned long long* m1 = sc.get<unsigned long long>(n);
+  int* left = sc.get<int>(2);
+  CUDA_CHECK(cudaMemsetAsync(und, 1, n, s));
+  CUDA_CHECK(cudaMemsetAsync(root, 0, n, s));
+  for (int round = 0; round <= n; ++round) {
+    k_mis_min1<<<nblk(n), kSB, 0, s>>>(n, A.ptr, A.col, und, hashed, m1);
+    k_mis_min2<<<nblk(n), kSB, 0, s>>>(n, A.ptr, A.col, und, hashed, m1, fresh, root);
+    k_mis_spread<<<nblk(n), kSB, 0, s>>>(n, A.ptr, A.col, fresh, d1);
+    k_mis_spread<<<nblk(n), kSB, 0, s>>>(n, A.ptr, A.col, d1, d2);
+    CUDA_CHECK(cudaMemsetAsync(left, 0, sizeof(int), s));
+    k_mis_retire<<<nblk(n), kSB, 0, s>>>(n, d2, und, left);
+    CUDA_CHECK(cudaGetLastError());
+    if (d2h(left, s) == 0) break;
+  }
+  int* rf = sc.get<int>(n + 1);
+  int* ridx = sc.get<int>(n + 1);
+  k_root_flags<<<nblk(n), kSB, 0, s>>>(n, root, rf);
+  exclusive_scan<int>(rf, ridx, n, s);
+  const int nAgg = d2h(ridx + n, s);
+  int* a1 = sc.get<int>(n);
+  k_agg_step3<<<nblk(n), kSB, 0, s>>>(n, A.ptr, A.col, root, ridx, hashed, a1);
+  CUDA_CHECK(cudaMemsetAsync(left + 1, 0, sizeof(int), s));
+  k_agg_step4<<<nblk(n), kSB, 0, s>>>(n, A.ptr, A.col, a1, hashed, agg, left + 1);
+  CUDA_CHECK(cudaGetLastError());
+  if (d2h(left + 1, s) != 0) throw Error(LDU_ERR_STATE, "MIS-2 aggregation left a node unassigned");
+  return nAgg;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Lanczos estimate of rho(D^-1 A) (reading Z27)
+// ---------------------------------------------------------------------------------------------
+// fixed-order dot products: per-block partials, then one block sums them in index order
+template <int NV>
+__device__ __forceinline__ void block_store(double (&v)[NV], double* part) {
+  __shared__ double sm[NV][32];
+  block_reduce<NV>(v, sm);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) part[k * gridDim.x + blockIdx.x] = v[k];
+}
+
+__global__ void k_sum_parts(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+  __shared__ double sm[1][32];
+  double v[1];
+  sum_slots<1>(part, nparts, nparts, v);
+  block_reduce<1>(v, sm);
+  if (threadIdx.x == 0) out[0] = v[0];
+}
+
+// v0_i = mix32(i) / 2^32 - 1/2; s_i = 1 / sqrt(a_ii); partial sum v^2
+__global__ void k_lz_init(int n, const double* __restrict__ diag, double* __restrict__ v,
+                          double* __restrict__ sd, double* part) {
+  double a[1] = {0.0};
+  GSTRIDE(i, n) {
+    const double vi = (double)amg_mix32((unsigned)i) / 4294967296.0 - 0.5;
+    v[i] = vi;
+    sd[i] = 1.0 / sqrt(diag[i]);
+    a[0] += vi * vi;
+  }
+  block_store<1>(a, part);
+}
+
+__global__ void k_lz_scale(int n, double* __restrict__ v, const double* __restrict__ nrm2) {
+  const double nr = sqrt(*nrm2);
+  GSTRIDE(i, n) v[i] = v[i] / nr;
+}
+
+// w = s .* (A (s .* v)) - beta v_prev; partial (w, v)
+__global__ void k_lz_matvec(CsrView A, const double* __restrict__ sd, const double* __restrict__ v,
+                            const double* __restrict__ vprev, const double* __restrict__ beta,
+                            double* __restrict__ w, double* part) {
+  const double b = *beta;
+  double a[1] = {0.0};
+  GSTRIDE(i, A.n) {
+    double acc = 0.0;
+    for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+      const int j = A.col[k];
+      acc += A.val[k] * (sd[j] * v[j]);
+    }
+    const double wi = sd[i] * acc - b * vprev[i];
+    w[i] = wi;
+    a[0] += wi * v[i];
+  }
+  block_store<1>(a, part);
+}
+
+// w -= alpha v; partial (w, w)
+__global__ void k_lz_orth(int n, double* __restrict__ w, const double* __restrict__ v,
+                          const double* __restrict__ alpha, double* part) {
+  const double al = *alpha;
+  double a[1] = {0.0};
+  GSTRIDE(i, n) {
+    const double wi = w[i] - al * v[i];
+    w[i] = wi;
+    a[0] += wi * wi;
+  }
+  block_store<1>(a, part);
+}
+
+// v_prev = v; v = w / beta
+__global__ void k_lz_next(int n, double* __restrict__ vprev, double* __restrict__ v,
+                          const double* __restrict__ w, const double* __restrict__ beta) {
+  const double b = *beta;
+  GSTRIDE(i, n) {
+    vprev[i] = v[i];
+    v[i] = w[i] / b;
+  }
+}
+
+__global__ void k_sqrt(double* x) { x[0] = sqrt(x[0]); }
+
+// largest eigenvalue of the symmetric tridiagonal (alpha[0..m), beta[0..m-1)) by bisection on
+// the Sturm count; then w = (4/3) / (1.05 lambda) (reading Z27)
+__global__ void k_tridiag_max(int m, const double* __restrict__ al, const double* __restrict__ be,
+                              double* __restrict__ out) {
+  if (threadIdx.x || blockIdx.x) return;
+  double lo = al[0], hi = al[0];
+  for (int i = 0; i < m; ++i) {
+    const double r = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < m ? fabs(be[i]) : 0.0);
+    lo = fmin(lo, al[i] - r);
+    hi = fmax(hi, al[i] + r);
+  }
+  // count(x) = number of eigenvalues < x
+  auto count = [&](double x) {
+    int c = 0;
+    double d = al[0] - x;
+    if (d < 0) ++c;
+    for (int i = 1; i < m; ++i) {
+      if (d == 0.0) d = 1e-300;
+      d = al[i] - x - be[i - 1] * be[i - 1] / d;
+      if (d < 0) ++c;
+    }
+    return c;
+  };
+  double a = lo, b = hi;  // invariant: count(a) < m, count(b) == m (largest eigenvalue in [a, b])
+  b = hi + fabs(hi) * 1e-15 + 1e-300;
+  for (int it = 0; it < 400; ++it) {
+    const double mid = 0.5 * (a + b);
+    if (mid <= a || mid >= b) break;
+    if (count(mid) == m) b = mid;
+    else a = mid;
+  }
+  const double lam = 0.5 * (a + b);
+  out[0] = lam;
+  out[1] = (4.0 / 3.0) / (1.05 * lam);
+}
+
+double lanczos_omega(const CsrMat& A, const double* diag, int steps, cudaStream_t s,
+                     double* ritzOut) {
+  Scratch sc;
+  const int n = A.nrows;
+  const int G = nblk(n);
+  double* v = sc.get<double>(n);
+  double* vp = sc.get<double>(n);
+  double* w = sc.get<double>(n);
+  double* sd = sc.get<double>(n);
+  double* part = sc.get<double>(G);
+  const int ms = std::min(steps, n);
+  double* al = sc.get<double>(ms + 1);
+  double* be = sc.get<double>(ms + 1);
+  double* scal = sc.get<double>(4);  // [0] |v|^2, [1] beta (current), [2..3] result
+  k_lz_init<<<G, kSB, 0, s>>>(n, diag, v, sd, part);
+  k_sum_parts<<<1, kSB, 0, s>>>(part, G, scal);
+  k_lz_scale<<<G, kSB, 0, s>>>(n, v, scal);
+  CUDA_CHECK(cudaMemsetAsync(vp, 0, sizeof(double) * n, s));
+  CUDA_CHECK(cudaMemsetAsync(scal + 1, 0, sizeof(double), s));
+  int m = 0;
+  for (int j = 0; j < ms; ++j) {
+    k_lz_matvec<<<G, kSB, 0, s>>>(view(A), sd, v, vp, scal + 1, w, part);
+    k_sum_parts<<<1, kSB, 0, s>>>(part, G, al + j);
+    k_lz_orth<<<G, kSB, 0, s>>>(n, w, v, al + j, part);
+    k_sum_parts<<<1, kSB, 0, s>>>(part, G, be + j);
+    k_sqrt<<<1, 1, 0, s>>>(be + j);
+    CUDA_CHECK(cudaGetLastError());
+    m = j + 1;
+    const double bj = d2h(be + j, s);
+    if (bj == 0.0 || j == ms - 1) break;
+    CUDA_CHECK(cudaMemcpyAsync(scal + 1, be + j, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    k_lz_next<<<G, kSB, 0, s>>>(n, vp, v, w, be + j);
+  }
+  k_tridiag_max<<<1, 1, 0, s>>>(m, al, be, scal + 2);
+  CUDA_CHECK(cudaGetLastError());
+  double res[2];
+  CUDA_CHECK(cudaMemcpyAsync(res, scal + 2, sizeof(res), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  if (ritzOut) *ritzOut = res[0];
+  if (!(res[0] > 0.0) || !std::isfinite(res[1]))
+    throw Error(LDU_ERR_STATE, "AMG: Lanczos estimate of rho(D^-1 A) is not positive");
+  return res[1];
+}
+
+// ---------------------------------------------------------------------------------------------
+// prolongator, restriction, Galerkin product
+// ---------------------------------------------------------------------------------------------
+__global__ void k_diag_of(CsrView A, double* __restrict__ diag, double* __restrict__ rD,
+                          int* __restrict__ bad) {
+  GSTRIDE(i, A.n) {
+    double d = 0.0;
+    for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
+      if (A.col[k] == i) d += A.val[k];
+    diag[i] = d;
+    rD[i] = 1.0 / d;
+    if (!(d > 0.0) || !isfinite(d)) atomicAdd(bad, 1);
+  }
+}
+
+// S = A T expansion (smoothed) or T (unsmoothed): row i, key (i, agg[j]) in A's column order
+__global__ void k_expand_AT(CsrView A, int nAgg, const int* __restrict__ agg,
+                            unsigned long long* __restrict__ key, double* __restrict__ val) {
+  GSTRIDE(i, A.n) {
+    const unsigned long long rk = (unsigned long long)i * nAgg;
+    for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+      key[k] = rk + agg[A.col[k]];
+      val[k] = A.val[k];
+    }
+  }
+}
+
+__global__ void k_expand_T(int n, int nAgg, const int* __restrict__ agg,
+                           unsigned long long* __restrict__ key, double* __restrict__ val) {
+  GSTRIDE(i, n) {
+    key[i] = (unsigned long long)i * nAgg + agg[i];
+    val[i] = 1.0;
+  }
+}
+
+// P_iJ = T_iJ - (w / a_ii) S_iJ   (oracle: T - diags(w / A.diagonal()) @ (A @ T))
+__global__ void k_finish_P(CsrView S, const int* __restrict__ agg, const double* __restrict__ diag,
+                           double omega, double* __restrict__ val, int* __restrict__ zeros) {
+  GSTRIDE(i, S.n) {
+    const double f = omega / diag[i];
+    int z = 0;
+    for (int k = S.ptr[i]; k < S.ptr[i + 1]; ++k) {
+      const double t = (S.col[k] == agg[i]) ? 1.0 : 0.0;
+      const double p = t - __dmul_rn(f, S.val[k]);  // two roundings, as T - (w/a_ii) S
+      val[k] = p;
+      z += (p == 0.0);
+    }
+    if (z) atomicAdd(zeros, z);
+  }
+}
+
+// drop exact zeros of a CSR in place (rare; only called when some exist)
+__global__ void k_nz_count(CsrView A, long long* __restrict__ cnt) {
+  GSTRIDE(i, A.n) {
+    long long c = 0;
+    for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) c += (A.val[k] != 0.0);
+    cnt[i] = c;
+  }
+}
+__global__ void k_nz_copy(CsrView A, const long long* __restrict__ off, int* __restrict__ col,
+                          double* __restrict__ val) {
+  GSTRIDE(i, A.n) {
+    long long o = off[i];
+    for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
+      if (A.val[k] != 0.0) {
+        col[o] = A.col[k];
+        val[o++] = A.val[k];
+      }
+  }
+}
+__global__ void k_l2i(long long n, const long long* __restrict__ a, int* __restrict__ b) {
+  GSTRIDE(i, n) b[i] = (int)a[i];
+}
+
+void drop_zeros(CsrMat& A, cudaStream_t s) {
+  Scratch sc;
+  long long* cnt = sc.get<long long>(A.nrows + 1);
+  long long* off = sc.get<long long>(A.nrows + 1);
+  k_nz_count<<<nblk(A.nrows), kSB, 0, s>>>(view(A), cnt);
+  exclusive_scan<long long>(cnt, off, A.nrows, s);
+  const long long nnz = d2h(off + A.nrows, s);
+  int* col = dmalloc<int>(nnz);
+  double* val = dmalloc<double>(nnz);
+  k_nz_copy<<<nblk(A.nrows), kSB, 0, s>>>(view(A), off, col, val);
+  int* ptr = dmalloc<int>(A.nrows + 1);
+  k_l2i<<<nblk(A.nrows + 1), kSB, 0, s>>>(A.nrows + 1, off, ptr);
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  A.release();
+  A.ptr = ptr;
+  A.col = col;
+  A.val = val;
+  A.nnz = nnz;
+  A.group = group_of(nnz, A.nrows);
+}
+
+// transpose expansion: P entry (i, J, p) -> key (J, i)
+__global__ void k_expand_T_of(CsrView P, int nrowsT, unsigned long long* __restrict__ key,
+                              double* __restrict__ val) {
+  GSTRIDE(i, P.n) {
+    for (int k = P.ptr[i]; k < P.ptr[i + 1]; ++k) {
+      key[k] = (unsigned long long)P.col[k] * (unsigned long long)P.n + i;
+      val[k] = P.val[k];
+    }
+  }
+}
+
+// expansion sizes of A P: row i -> sum over A's entries (i, j) of |P_j|
+__global__ void k_count_AP(CsrView A, const int* __restrict__ Pptr, long long* __restrict__ cnt) {
+  GSTRIDE(i, A.n) {
+    long long c = 0;
+    for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+      const int j = A.col[k];
+      c += Pptr[j + 1] - Pptr[j];
+    }
+    cnt[i] = c;
+  }
+}
+__global__ void k_expand_AP(CsrView A, CsrView P, int ncols, const long long* __restrict__ off,
+                            unsigned long long* __restrict__ key, double* __restrict__ val) {
+  GSTRIDE(i, A.n) {
+    long long o = off[i];
+    const unsigned long long rk = (unsigned long long)i * ncols;
+    for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+      const int j = A.col[k];
+      const double a = A.val[k];
+      for (int t = P.ptr[j]; t < P.ptr[j + 1]; ++t) {
+        key[o] = rk + P.col[t];
+        val[o++] = a * P.val[t];
+      }
+    }
+  }
+}
+
+// expansion of P^T (A P): row i of P and of AP -> (I, J) += p_iI * ap_iJ
+__global__ void k_count_PtAP(int n, const int* __restrict__ Pptr, const int* __restrict__ Qptr,
+                             long long* __restrict__ cnt) {
+  GSTRIDE(i, n) cnt[i] = (long long)(Pptr[i + 1] - Pptr[i]) * (Qptr[i + 1] - Qptr[i]);
+}
+__global__ void k_expand_PtAP(CsrView P, CsrView Q, int nc, const long long* __restrict__ off,
+                              unsigned long long* __restrict__ key, double* __restrict__ val) {
+  GSTRIDE(i, P.n) {
+    long long o = off[i];
+    for (int m = P.ptr[i]; m < P.ptr[i + 1]; ++m) {
+      const unsigned long long rk = (unsigned long long)P.col[m] * nc;
+      const double p = P.val[m];
+      for (int t = Q.ptr[i]; t < Q.ptr[i + 1]; ++t) {
+        key[o] = rk + Q.col[t];
+        val[o++] = p * Q.val[t];
+      }
+    }
+  }
+}
+
+CsrMat build_P(const CsrMat& A, const int* agg, int nAgg, const double* diag, double omega,
+               bool smooth, cudaStream_t s) {
+  Scratch sc;
+  const int n = A.nrows;
+  if (!smooth) {
+    unsigned long long* key = sc.get<unsigned long long>(n);
+    double* val = sc.get<double>(n);
+    k_expand_T<<<nblk(n), kSB, 0, s>>>(n, nAgg, agg, key, val);
+    return assemble(n, nAgg, n, key, val, false, s);
+  }
+  unsigned long long* key = sc.get<unsigned long long>(A.nnz);
+  double* val = sc.get<double>(A.nnz);
+  k_expand_AT<<<nblk(n), kSB, 0, s>>>(view(A), nAgg, agg, key, val);
+  CsrMat P = assemble(n, nAgg, A.nnz, key, val, false, s);  // S = A T
+  int* zeros = sc.get<int>(1);
+  CUDA_CHECK(cudaMemsetAsync(zeros, 0, sizeof(int), s));
+  k_finish_P<<<nblk(n), kSB, 0, s>>>(view(P), agg, diag, omega, P.val, zeros);
+  CUDA_CHECK(cudaGetLastError());
+  if (d2h(zeros, s)) drop_zeros(P, s);
+  return P;
+}
+
+CsrMat transpose(const CsrMat& P, cudaStream_t s) {
+  Scratch sc;
+  unsigned long long* key = sc.get<unsigned long long>(P.nnz);
+  double* val = sc.get<double>(P.nnz);
+  k_expand_T_of<<<nblk(P.nrows), kSB, 0, s>>>(view(P), P.ncols, key, val);
+  return assemble(P.ncols, P.nrows, P.nnz, key, val, false, s);
+}
+
+CsrMat galerkin(const CsrMat& A, const CsrMat& P, cudaStream_t s) {
+  const int n = A.nrows, nc = P.ncols;
+  CsrMat AP;
+  {
+    Scratch sc;
+    long long* cnt = sc.get<long long>(n + 1);
+    long long* off = sc.get<long long>(n + 1);
+    k_count_AP<<<nblk(n), kSB, 0, s>>>(view(A), P.ptr, cnt);
+    exclusive_scan<long long>(cnt, off, n, s);
+    const long long m = d2h(off + n, s);
+    unsigned long long* key = sc.get<unsigned long long>(m);
+    double* val = sc.get<double>(m);
+    k_expand_AP<<<nblk(n), kSB, 0, s>>>(view(A), view(P), nc, off, key, val);
+    AP = assemble(n, nc, m, key, val, true, s);
+  }
+  CsrMat Ac;
+  {
+    Scratch sc;
+    long long* cnt = sc.get<long long>(n + 1);
+    long long* off = sc.get<long long>(n + 1);
+    k_count_PtAP<<<nblk(n), kSB, 0, s>>>(n, P.ptr, AP.ptr, cnt);
+    exclusive_scan<long long>(cnt, off, n, s);
+    const long long m = d2h(off + n, s);
+    unsigned long long* key = sc.get<unsigned long long>(m);
+    double* val = sc.get<double>(m);
+    k_expand_PtAP<<<nblk(n), kSB, 0, s>>>(view(P), view(AP), nc, off, key, val);
+    AP.release();
+    Ac = assemble(nc, nc, m, key, val, true, s);
+  }
+  return Ac;
+}
+
+// ---------------------------------------------------------------------------------------------
+// coarsest level: dense Gauss-Jordan inverse (SPD, no pivoting; reading Z31)
+// ---------------------------------------------------------------------------------------------
+__global__ void k_dense_of(CsrView A, double* __restrict__ D, double* __restrict__ I) {
+  GSTRIDE(i, A.n) {
+    for (int j = 0; j < A.n; ++j) {
+      D[i * A.n + j] = 0.0;
+      I[i * A.n + j] = (i == j) ? 1.0 : 0.0;
+    }
+    for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) D[i * A.n + A.col[k]] += A.val[k];
+  }
+}
+
+__global__ void k_gj_pivot(int n, int k, double* __restrict__ D, double* __restrict__ I,
+                           double* __restrict__ fac, int* __restrict__ bad) {
+  const double piv = D[(long long)k * n + k];
+  if (!(piv > 0.0) || !isfinite(piv)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(bad, 1);
+  }
+  GSTRIDE(t, n) {
+    fac[t] = (t == k) ? 0.0 : D[t * n + k];
+  }
+  __syncthreads();
+  // row k scaled (after every fac read of column k in this grid: separate launch not needed
+  // because only row k is written and fac[k] is not read from D)
+  GSTRIDE(j, n) {
+    D[(long long)k * n + j] /= piv;
+    I[(long long)k * n + j] /= piv;
+  }
+}
+
+__global__ void k_gj_elim(int n, int k, double* __restrict__ D, double* __restrict__ I,
+                          const double* __restrict__ fac) {
+  GSTRIDE(t, (long long)n * n) {
+    const long long i = t / n, j = t % n;
+    if (i == k) continue;
+    const double f = fac[i];
+    D[t] -= f * D[(long long)k * n + j];
+    I[t] -= f * I[(long long)k * n + j];
+  }
+}
+
+double* dense_inverse(const CsrMat& A, cudaStream_t s) {
+  Scratch sc;
+  const int n = A.nrows;
+  double* D = sc.get<double>((size_t)n * n);
+  double* I = dmalloc<double>((size_t)n * n);
+  double* fac = sc.get<double>(n);
+  int* bad = sc.get<int>(1);
+  CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  k_dense_of<<<nblk(n), kSB, 0, s>>>(view(A), D, I);
+  for (int k = 0; k < n; ++k) {
+    // single block: the column-k reads and the row-k writes are ordered by __syncthreads
+    k_gj_pivot<<<1, 1024, 0, s>>>(n, k, D, I, fac, bad);
+    k_gj_elim<<<nblk((long long)n * n), kSB, 0, s>>>(n, k, D, I, fac);
+  }
+  CUDA_CHECK(cudaGetLastError());
+  if (d2h(bad, s)) {
+    dfree(I);
+    throw Error(LDU_ERR_STATE, "AMG: coarsest matrix is not positive definite");
+  }
+  return I;
+}
+
+void free_level(AmgLevel& L) {
+  L.A.release();
+  L.P.release();
+  L.R.release();
+  if (L.ownsDiag) {
+    dfree(L.diag);
+    dfree(L.rD);
+  }
+  for (void* p : {(void*)L.agg, (void*)L.r, (void*)L.x, (void*)L.f, (void*)L.z}) dfree(p);
+  L = AmgLevel{};
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// public-internal entry points
+// ---------------------------------------------------------------------------------------------
+void amg_release(ldu_handle h) {
+  AmgHierarchy* H = h->amg;
+  if (!H) return;
+  cudaSetDevice(h->device);
+  if (h->own_stream) cudaStreamSynchronize(h->own_stream);
+  for (cudaGraphExec_t g : H->graph)
+    if (g) cudaGraphExecDestroy(g);
+  for (AmgLevel& L : H->lv) free_level(L);
+  H->Ac.release();
+  for (void* p : {(void*)H->Ainv, (void*)H->fL, (void*)H->zL, (void*)H->u, (void*)H->m,
+                  (void*)H->zk, (void*)H->qk})
+    dfree(p);
+  delete H;
+  h->amg = nullptr;
+}
+
+void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
+  ldu_amg_opts o{};
+  if (opts) o = *opts;
+  if (o.reserved[0] || o.reserved[1] || o.reserved[2]) fail_arg("ldu_amg_opts.reserved must be zero");
+  if (o.coarsest < 0 || o.maxLevels < 0 || o.lanczosSteps < 0) fail_arg("negative AMG option");
+  if (o.keyIndexOrder != 0 && o.keyIndexOrder != 1) fail_arg("keyIndexOrder must be 0 or 1");
+  if (o.unsmoothed != 0 && o.unsmoothed != 1) fail_arg("unsmoothed must be 0 or 1");
+  if (o.maxLevels > LDU_AMG_MAX_LEVELS) fail_arg("maxLevels > LDU_AMG_MAX_LEVELS");
+  if (!o.coarsest) o.coarsest = 64;
+  if (!o.maxLevels) o.maxLevels = LDU_AMG_MAX_LEVELS;
+  if (!o.lanczosSteps) o.lanczosSteps = 20;
+  if (!h->symmetric) fail_arg("AMG requires a symmetric matrix (lower == NULL or lower == upper)");
+  if (h->comm && h->comm->nRanks > 1)
+    throw Error(LDU_ERR_STATE, "AMG on multi-rank handles is not supported yet (reading Z33)");
+  amg_release(h);
+  cudaStream_t s = h->own_stream;
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, h->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_fork, 0));
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev[0], s));
+  AmgHierarchy* H = new AmgHierarchy();
+  H->opts = o;
+  h->amg = H;
+  try {
+    const int hashed = o.keyIndexOrder ? 0 : 1;
+    CsrMat A = level0_csr(h, s);
+    double* diag = h->diag;
+    double* rD = h->rD;
+    bool owns = false;
+    while (A.nrows > o.coarsest && (int)H->lv.size() < o.maxLevels) {
+      const int n = A.nrows;
+      int* agg = dmalloc<int>(n);
+      const int nAgg = mis2_aggregate(A, hashed, agg, s);
+      if (nAgg >= n) {  // no coarsening possible (Z31)
+        dfree(agg);
+        break;
+      }
+      AmgLevel L;
+      L.n = n;
+      L.nc = nAgg;
+      L.A = A;
+      L.diag = diag;
+      L.rD = rD;
+      L.ownsDiag = owns;
+      L.agg = agg;
+      L.omega = lanczos_omega(A, diag, o.lanczosSteps, s, nullptr);
+      L.P = build_P(A, agg, nAgg, diag, L.omega, !o.unsmoothed, s);
+      L.R = transpose(L.P, s);
+      CsrMat Ac = galerkin(A, L.P, s);
+      L.r = dmalloc<double>(n);
+      L.x = dmalloc<double>(n);
+      if (!H->lv.empty()) {
+        L.f = dmalloc<double>(n);
+        L.z = dmalloc<double>(n);
+      }
+      H->lv.push_back(L);
+      // next level's diagonal
+      diag = dmalloc<double>(Ac.nrows);
+      rD = dmalloc<double>(Ac.nrows);
+      owns = true;
+      {
+        Scratch sc;
+        int* bad = sc.get<int>(1);
+        CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+        k_diag_of<<<nblk(Ac.nrows), kSB, 0, s>>>(view(Ac), diag, rD, bad);
+        CUDA_CHECK(cudaGetLastError());
+        if (d2h(bad, s)) {
+          dfree(diag);
+          dfree(rD);
+          Ac.release();
+          throw Error(LDU_ERR_STATE, "AMG: coarse matrix with a non-positive diagonal");
+        }
+      }
+      A = Ac;
+    }
+    H->L = (int)H->lv.size();
+    H->nc = A.nrows;
+    if (H->nc > 8192) {
+      A.release();
+      if (owns) {
+        dfree(diag);
+        dfree(rD);
+      }
+      fail_arg("AMG: coarsest level has " + std::to_string(H->nc) + " rows (> 8192 for the dense solve)");
+    }
+    H->Ainv = dense_inverse(A, s);
+    H->Ac = A;  // level L (for L == 0 this is the level-0 CSR itself)
+    if (owns) {
+      dfree(diag);
+      dfree(rD);
+    }
+    if (H->L > 0) {
+      H->fL = dmalloc<double>(H->nc);
+      H->zL = dmalloc<double>(H->nc);
+    }
+    CUDA_CHECK(cudaEventRecord(h->ev[1], s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+    H->setupMs = ms;
+  } catch (...) {
+    amg_release(h);
+    throw;
+  }
+}
+
+void amg_info(ldu_handle h, ldu_amg_info* out) {
+  AmgHierarchy* H = h->amg;
+  if (!H) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+  std::memset(out, 0, sizeof(*out));
+  out->nLevels = H->L;
+  out->coarsestN = H->nc;
+  long long bytes = 8LL * H->nc * H->nc, nnz0 = 0, tot = 0;
+  for (int l = 0; l < H->L; ++l) {
+    const AmgLevel& L = H->lv[l];
+    out->n[l] = L.n;
+    out->nnzA[l] = L.A.nnz;
+    out->nnzP[l] = L.P.nnz;
+    out->omega[l] = L.omega;
+    tot += L.A.nnz;
+    bytes += 12LL * (L.A.nnz + L.P.nnz + L.R.nnz) + 4LL * (2 * L.n + L.nc + 3) + 8LL * 2 * L.n +
+             4LL * L.n + (l ? 8LL * 4 * L.n : 0);
+  }
+  out->n[H->L] = H->nc;
+  out->nnzA[H->L] = H->Ac.nnz;
+  tot += H->Ac.nnz;
+  nnz0 = H->L ? H->lv[0].A.nnz : H->Ac.nnz;
+  out->operatorComplexity = nnz0 ? (double)tot / nnz0 : 0.0;
+  out->setupMs = H->setupMs;
+  out->deviceBytes = bytes + 12LL * H->Ac.nnz;
+}
+
+void amg_export(ldu_handle h, int level, int which, int* ptr, int* col, double* val) {
+  AmgHierarchy* H = h->amg;
+  if (!H) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+  if (which < 0 || which > 2) fail_arg("which must be 0 (A), 1 (P) or 2 (R)");
+  const int maxLevel = which == 0 ? H->L : H->L - 1;
+  if (level < 0 || level > maxLevel) fail_arg("level out of range");
+  const CsrMat& M = which == 0 ? (level == H->L ? H->Ac : H->lv[level].A)
+                               : (which == 1 ? H->lv[level].P : H->lv[level].R);
+  if (ptr) CUDA_CHECK(cudaMemcpy(ptr, M.ptr, sizeof(int) * (M.nrows + 1), cudaMemcpyDefault));
+  if (col) CUDA_CHECK(cudaMemcpy(col, M.col, sizeof(int) * M.nnz, cudaMemcpyDefault));
+  if (val) CUDA_CHECK(cudaMemcpy(val, M.val, sizeof(double) * M.nnz, cudaMemcpyDefault));
+}
+
+void amg_export_agg(ldu_handle h, int level, int* agg) {
+  AmgHierarchy* H = h->amg;
+  if (!H) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+  if (level < 0 || level >= H->L) fail_arg("level out of range");
+  if (!agg) fail_arg("agg is NULL");
+  CUDA_CHECK(cudaMemcpy(agg, H->lv[level].agg, sizeof(int) * H->lv[level].n, cudaMemcpyDefault));
+}
+
+}  // namespace ldu

@@ -1,0 +1,586 @@
+// ldu_amg_solve.cuh -- V-cycle and AMG-preconditioned CG / pipelined CG (NEXT-2; P:236,
+// Table 2).  Included at the end of ldu_solve.cu: it shares that translation unit's
+// helpers (layout dispatch, reductions, r0, graph plumbing).
+//
+// V-cycle z = B f (reading Z32), level l < L with A_l, P_l, R_l, w_l, rD_l:
+//   K1  r_l = f_l - A_l (w rD f_l)                 pre-sweep from x = 0 fused with the residual
+//   K2  f_{l+1} = R_l r_l                          restriction
+//       ... level l+1 ...   (level L: z_L = A_L^-1 f_L, dense inverse)
+//   K3  x_l = w rD f_l + P_l z_{l+1}               prolongation added to the pre-sweep iterate
+//   K4  z_l = x_l + w rD (f_l - A_l x_l)           post-sweep
+// Level 0 runs K1 / K4 on the handle's own layout (DIA / SELL-32, one row per thread); coarser
+// levels and every P / R are CSR with a sub-warp of `group` lanes per row (fixed-order shuffle
+// reduction: deterministic).
+//
+// AMG-PCG, iteration k (SURVEY §8(c) c2 with z = B r):
+//   V-cycle z_k = B r_k, K4 of level 0 carries the partial (z_k, r_k)   -> ctl: beta_k
+//   pass A: x += alpha_{k-1} p_{k-1}; p_k = z_k + beta_k p_{k-1} (recomputed at the neighbours,
+//           ping-pong); q = A p_k; partial (p_k, q)                       -> ctl: alpha_k
+//   pass B: r -= alpha_k q; partial crit(r)                                -> ctl: test
+// AMG-PipeCG, iteration i (c3 literal Ghysels-Vanroose, u = B r, m = B w):
+//   V-cycle m_i = B w_i
+//   pass SU: n = A m (row by row, never stored); z = n + b z; q = m + b q; s = w + b s;
+//            p = u + b p; x += a p; r -= a s; u -= a q; w -= a z; partials (r,u), (w,u), crit(r)
+//                                                                          -> ctl: a, b, test
+#pragma once
+
+#include "ldu_amg.cuh"
+
+namespace ldu {
+namespace {
+
+// ---- CSR-vector rows: `G` lanes per row, grid-stride over warps -------------------------------
+template <int G, class Epi>
+__global__ void __launch_bounds__(kBlock) k_csr_vec(CsrView A, Epi e, const State* st) {
+  if (st && st->done) return;
+  constexpr int RPW = 32 / G;  // rows per warp
+  const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long base = warp * RPW; base < A.n; base += nwarps * RPW) {
+    const int row = (int)(base + lane / G);
+    double s = 0.0;
+    if (row < A.n) {
+      const int end = __ldg(A.ptr + row + 1);
+      for (int k = __ldg(A.ptr + row) + sub; k < end; k += G)
+        s = fma(__ldg(A.val + k), e.in(__ldg(A.col + k)), s);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (sub == 0 && row < A.n) e.out(row, s);
+  }
+}
+
+struct EpiPre {  // K1: r = f - A (w rD f)
+  double w;
+  const double* __restrict__ rD;
+  const double* __restrict__ f;
+  double* __restrict__ r;
+  __device__ __forceinline__ double in(int j) const { return w * __ldg(rD + j) * __ldg(f + j); }
+  __device__ __forceinline__ void out(int i, double s) const { r[i] = f[i] - s; }
+};
+struct EpiCopy {  // K2: y = M x
+  const double* __restrict__ x;
+  double* __restrict__ y;
+  __device__ __forceinline__ double in(int j) const { return __ldg(x + j); }
+  __device__ __forceinline__ void out(int i, double s) const { y[i] = s; }
+};
+struct EpiProlong {  // K3: x = w rD f + P xc
+  double w;
+  const double* __restrict__ rD;
+  const double* __restrict__ f;
+  const double* __restrict__ xc;
+  double* __restrict__ x;
+  __device__ __forceinline__ double in(int j) const { return __ldg(xc + j); }
+  __device__ __forceinline__ void out(int i, double s) const { x[i] = w * rD[i] * f[i] + s; }
+};
+struct EpiPost {  // K4: z = x + w rD (f - A x)
+  double w;
+  const double* __restrict__ rD;
+  const double* __restrict__ f;
+  const double* __restrict__ x;
+  double* __restrict__ z;
+  __device__ __forceinline__ double in(int j) const { return __ldg(x + j); }
+  __device__ __forceinline__ void out(int i, double s) const { z[i] = x[i] + w * rD[i] * (f[i] - s); }
+};
+
+int csr_grid(long long rows, int G) {
+  const long long warps = (rows + 32 / G - 1) / (32 / G);
+  const long long b = (warps * 32 + kBlock - 1) / kBlock;
+  return (int)std::max(1LL, std::min(b, 148LL * 16));
+}
+
+template <class Epi>
+void launch_csr(const CsrMat& M, const Epi& e, const State* st, cudaStream_t s) {
+  const CsrView v = view(M);
+  const int g = csr_grid(M.nrows, M.group);
+  switch (M.group) {
+    case 1: k_csr_vec<1><<<g, kBlock, 0, s>>>(v, e, st); break;
+    case 2: k_csr_vec<2><<<g, kBlock, 0, s>>>(v, e, st); break;
+    case 4: k_csr_vec<4><<<g, kBlock, 0, s>>>(v, e, st); break;
+    case 8: k_csr_vec<8><<<g, kBlock, 0, s>>>(v, e, st); break;
+    case 16: k_csr_vec<16><<<g, kBlock, 0, s>>>(v, e, st); break;
+    default: k_csr_vec<32><<<g, kBlock, 0, s>>>(v, e, st); break;
+  }
+}
+
+// ---- level 0 on the handle's layout -----------------------------------------------------------
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_vc_pre(Fmt A, const double* __restrict__ diag,
+                                                   const double* __restrict__ rD, double w,
+                                                   const double* __restrict__ f,
+                                                   double* __restrict__ r, const State* st) {
+  if (st && st->done) return;
+  GRID_STRIDE(c, A.n) {
+    const double fc = __ldg(f + c);
+    const double xc = w * __ldg(rD + c) * fc;
+    const double ax = row_apply(A, c, __ldg(diag + c) * xc,
+                                [&](int j) { return w * __ldg(rD + j) * __ldg(f + j); });
+    r[c] = fc - ax;
+  }
+}
+
+// K4 at level 0; RHO: partial (z, f) for the classical control step
+template <class Fmt, bool RHO>
+__global__ void __launch_bounds__(kBlock) k_vc_post(Fmt A, const double* __restrict__ diag,
+                                                    const double* __restrict__ rD, double w,
+                                                    const double* __restrict__ f,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ z, State* st, Red rd) {
+  if (st && st->done) return;
+  double v[1] = {0.0};
+  GRID_STRIDE(c, A.n) {
+    const double xc = __ldg(x + c), fc = __ldg(f + c);
+    const double ax = row_apply(A, c, __ldg(diag + c) * xc, [&](int j) { return __ldg(x + j); });
+    const double zc = xc + w * __ldg(rD + c) * (fc - ax);
+    z[c] = zc;
+    if (RHO) v[0] = fma(zc, fc, v[0]);
+  }
+  if (RHO) finish_reduction<1>(v, rd, st);
+}
+
+// coarsest level: z = Ainv f, one warp per row
+__global__ void __launch_bounds__(kBlock) k_dense_mv(int n, const double* __restrict__ Ainv,
+                                                     const double* __restrict__ f,
+                                                     double* __restrict__ z, const State* st) {
+  if (st && st->done) return;
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long i = warp; i < n; i += nwarps) {
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(Ainv[i * n + j], f[j], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) z[i] = s;
+  }
+}
+
+// (a, b) partial -> control step (used when the hierarchy has no level below 0)
+__global__ void __launch_bounds__(kBlock) k_amg_dot(int n, const double* __restrict__ a,
+                                                    const double* __restrict__ b, State* st,
+                                                    Red rd) {
+  if (st->done) return;
+  double v[1] = {0.0};
+  GRID_STRIDE(c, n) v[0] = fma(a[c], b[c], v[0]);
+  finish_reduction<1>(v, rd, st);
+}
+
+// ---- Krylov passes ----------------------------------------------------------------------------
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_amg_passA(Fmt A, const double* __restrict__ diag,
+                                                      const double* __restrict__ z, double* p0,
+                                                      double* p1, double* __restrict__ q,
+                                                      double* __restrict__ x, State* st, Red rd) {
+  if (st->done) return;
+  const int k = st->k;
+  const double beta = st->beta, alpha = st->alpha;
+  const double* __restrict__ pold = (k & 1) ? p0 : p1;
+  double* __restrict__ pnew = (k & 1) ? p1 : p0;
+  double v[1] = {0.0};
+  GRID_STRIDE(c, A.n) {
+    const double po = __ldg(pold + c);
+    const double pc = fma(beta, po, __ldg(z + c));
+    const double qc = row_apply(A, c, __ldg(diag + c) * pc,
+                                [&](int j) { return fma(beta, __ldg(pold + j), __ldg(z + j)); });
+    pnew[c] = pc;
+    q[c] = qc;
+    x[c] = fma(alpha, po, x[c]);
+    v[0] = fma(pc, qc, v[0]);
+  }
+  finish_reduction<1>(v, rd, st);
+}
+
+__global__ void __launch_bounds__(kBlock) k_amg_passB(int n, const double* __restrict__ q,
+                                                      double* __restrict__ r, State* st, Red rd) {
+  if (st->done) return;
+  const double alpha = st->alpha;
+  const bool l2 = st->norm == LDU_NORM_L2;
+  double v[1] = {0.0};
+  GRID_STRIDE(c, n) {
+    const double rc = fma(-alpha, q[c], r[c]);
+    r[c] = rc;
+    v[0] += l2 ? rc * rc : fabs(rc);
+  }
+  finish_reduction<1>(v, rd, st);
+}
+
+// pipelined: partials [gamma = (r, u), delta = (w, u), crit(r)]
+__global__ void __launch_bounds__(kBlock) k_amg_pipe_dots(int n, const double* __restrict__ r,
+                                                          const double* __restrict__ u,
+                                                          const double* __restrict__ w, State* st,
+                                                          Red rd) {
+  if (st->done) return;
+  const bool l2 = st->norm == LDU_NORM_L2;
+  double v[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(c, n) {
+    const double rc = r[c], uc = u[c];
+    v[0] = fma(rc, uc, v[0]);
+    v[1] = fma(w[c], uc, v[1]);
+    v[2] += l2 ? rc * rc : fabs(rc);
+  }
+  finish_reduction<3>(v, rd, st);
+}
+
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_amg_pipe_SU(
+    Fmt A, const double* __restrict__ diag, const double* __restrict__ m, double* __restrict__ z,
+    double* __restrict__ q, double* __restrict__ s, double* __restrict__ p, double* __restrict__ x,
+    double* __restrict__ r, double* __restrict__ u, double* __restrict__ w, State* st, Red rd) {
+  if (st->done) return;
+  const double a = st->pa, b = st->pb;
+  const bool l2 = st->norm == LDU_NORM_L2;
+  double v[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(c, A.n) {
+    const double mc = __ldg(m + c);
+    const double nc = row_apply(A, c, __ldg(diag + c) * mc, [&](int j) { return __ldg(m + j); });
+    const double zc = fma(b, z[c], nc);
+    const double qc = fma(b, q[c], mc);
+    const double sc = fma(b, s[c], w[c]);
+    const double pc = fma(b, p[c], u[c]);
+    z[c] = zc;
+    q[c] = qc;
+    s[c] = sc;
+    p[c] = pc;
+    x[c] = fma(a, pc, x[c]);
+    const double rc = fma(-a, sc, r[c]);
+    const double uc = fma(-a, qc, u[c]);
+    const double wc = fma(-a, zc, w[c]);
+    r[c] = rc;
+    u[c] = uc;
+    w[c] = wc;
+    v[0] = fma(rc, uc, v[0]);
+    v[1] = fma(wc, uc, v[1]);
+    v[2] += l2 ? rc * rc : fabs(rc);
+  }
+  finish_reduction<3>(v, rd, st);
+}
+
+// ---- V-cycle enqueue --------------------------------------------------------------------------
+// z0 = B f0 on stream s.  st != nullptr: every kernel exits at entry once the solve is done.
+// rho != nullptr: level-0 post-sweep (or the direct solve) also reduces (z0, f0) into rho's control.
+long long enqueue_vcycle(ldu_handle h, const double* f0, double* z0, cudaStream_t s, State* st,
+                         const Red* rho) {
+  AmgHierarchy* H = h->amg;
+  long long kernels = 0;
+  const int L = H->L;
+  for (int l = 0; l < L; ++l) {
+    AmgLevel& Lv = H->lv[l];
+    const double* f = l ? Lv.f : f0;
+    if (l == 0) {
+      with_format(h, [&](auto A) {
+        k_vc_pre<<<h->gridA, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f, Lv.r, st);
+      });
+    } else {
+      launch_csr(Lv.A, EpiPre{Lv.omega, Lv.rD, f, Lv.r}, st, s);
+    }
+    double* fc = (l + 1 == L) ? H->fL : H->lv[l + 1].f;
+    launch_csr(Lv.R, EpiCopy{Lv.r, fc}, st, s);
+    kernels += 2;
+  }
+  {
+    const double* f = L ? H->fL : f0;
+    double* z = L ? H->zL : z0;
+    const int g = (int)std::min<long long>(148LL * 8, ((long long)H->nc * 32 + kBlock - 1) / kBlock);
+    k_dense_mv<<<std::max(1, g), kBlock, 0, s>>>(H->nc, H->Ainv, f, z, st);
+    ++kernels;
+    if (L == 0 && rho) {
+      k_amg_dot<<<h->grid, kBlock, 0, s>>>(h->n, z0, f0, st, *rho);
+      ++kernels;
+    }
+  }
+  for (int l = L - 1; l >= 0; --l) {
+    AmgLevel& Lv = H->lv[l];
+    const double* f = l ? Lv.f : f0;
+    const double* xc = (l + 1 == L) ? H->zL : H->lv[l + 1].z;
+    launch_csr(Lv.P, EpiProlong{Lv.omega, Lv.rD, f, xc, Lv.x}, st, s);
+    if (l == 0) {
+      with_format(h, [&](auto A) {
+        if (rho)
+          k_vc_post<decltype(A), true><<<h->gridA, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f,
+                                                                   Lv.x, z0, st, *rho);
+        else
+          k_vc_post<decltype(A), false><<<h->gridA, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f,
+                                                                    Lv.x, z0, st, Red{});
+      });
+    } else {
+      launch_csr(Lv.A, EpiPost{Lv.omega, Lv.rD, f, Lv.x, Lv.z}, st, s);
+    }
+    kernels += 2;
+  }
+  return kernels;
+}
+
+void ensure_amg_work(ldu_handle h, bool pipelined) {
+  AmgHierarchy* H = h->amg;
+  const int n = h->n;
+  ensure_vec(h->x, n);
+  ensure_vec(h->r, n);
+  ensure_vec(h->ybuf, n);
+  ensure_vec(h->p0, n);
+  if (!pipelined) {
+    ensure_vec(h->p1, n);
+    ensure_vec(h->q, n);
+    ensure_vec(H->zk, n);
+  } else {
+    ensure_vec(h->w, n);
+    ensure_vec(h->z, n);
+    ensure_vec(h->s, n);
+    ensure_vec(h->nv, n);  // sumA of the OpenFOAM norm
+    ensure_vec(H->u, n);
+    ensure_vec(H->m, n);
+    ensure_vec(H->qk, n);
+  }
+}
+
+long long enqueue_amg_iters(ldu_handle h, bool pipelined, int batch, cudaStream_t s, bool profile) {
+  AmgHierarchy* H = h->amg;
+  long long kernels = 0;
+  for (int it = 0; it < batch; ++it) {
+    prof_mark(h, profile, 4 * it + 0, s);
+    if (!pipelined) {
+      const Red rr = red_of(h, CTL_AMG_RHO, true, H->L ? h->gridA : h->grid);
+      kernels += enqueue_vcycle(h, h->r, H->zk, s, h->st, &rr);
+      prof_mark(h, profile, 4 * it + 1, s);
+      prof_mark(h, profile, 4 * it + 2, s);
+      with_format(h, [&](auto A) {
+        k_amg_passA<<<h->gridA, kBlock, 0, s>>>(A, h->diag, H->zk, h->p0, h->p1, h->q, h->x,
+                                                h->st, red_of(h, CTL_CG_A, true, h->gridA));
+      });
+      k_amg_passB<<<h->grid, kBlock, 0, s>>>(h->n, h->q, h->r, h->st, red_of(h, CTL_AMG_B, true));
+      kernels += 2;
+    } else {
+      kernels += enqueue_vcycle(h, h->w, H->m, s, h->st, nullptr);
+      prof_mark(h, profile, 4 * it + 1, s);
+      prof_mark(h, profile, 4 * it + 2, s);
+      with_format(h, [&](auto A) {
+        k_amg_pipe_SU<<<h->gridA, kBlock, 0, s>>>(A, h->diag, H->m, h->z, H->qk, h->s, h->p0, h->x,
+                                                  h->r, H->u, h->w, h->st,
+                                                  red_of(h, CTL_PIPE_NEXT, true, h->gridA));
+      });
+      ++kernels;
+    }
+    prof_mark(h, profile, 4 * it + 3, s);
+  }
+  return kernels;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// public-internal entry points
+// ---------------------------------------------------------------------------------------------
+void amg_vcycle(ldu_handle h, const double* r, double* z) {
+  if (!h->amg) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+  if (!r || !z) fail_arg("r and z must not be NULL");
+  cudaStream_t s = h->own_stream;
+  h->stats = ldu_solve_stats{};
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, h->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_fork, 0));
+  }
+  const int n = h->n;
+  const bool rd = is_device_ptr(r), zd = is_device_ptr(z);
+  const double* rin = r;
+  double* zout = z;
+  if (!rd) {
+    ensure_vec(h->bbuf, n);
+    CUDA_CHECK(cudaMemcpyAsync(h->bbuf, r, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    h->stats.h2dBytes += 8LL * n;
+    rin = h->bbuf;
+  }
+  if (!zd) {
+    ensure_vec(h->ybuf, n);
+    zout = h->ybuf;
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev[0], s));
+  h->stats.kernels = enqueue_vcycle(h, rin, zout, s, nullptr, nullptr);
+  CUDA_CHECK(cudaEventRecord(h->ev[1], s));
+  if (!zd) {
+    CUDA_CHECK(cudaMemcpyAsync(z, zout, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    h->stats.d2hBytes += 8LL * n;
+  }
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+    CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_fork, 0));
+  }
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+  h->stats.solveMs = ms;
+  h->stats.iterMs = ms;
+}
+
+ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, double tol,
+                     int maxIter, const ldu_solve_opts* opts, int* nIter, double* finalRes) {
+  AmgHierarchy* H = h->amg;
+  if (!H) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+  if (multi(h)) throw Error(LDU_ERR_STATE, "AMG solves on multi-rank handles are not supported yet");
+  if (!b || !x) fail_arg("b and x must not be NULL");
+  if (!(tol >= 0.0)) fail_arg("tol must be >= 0");
+  if (maxIter < 0) fail_arg("maxIter must be >= 0");
+  ldu_solve_opts o{};
+  if (opts) {
+    o = *opts;
+    if (o.reserved || o.reserved2[0] != 0.0 || o.reserved2[1] != 0.0)
+      fail_arg("ldu_solve_opts.reserved must be zero");
+  }
+  if (!(o.relTol >= 0.0)) fail_arg("relTol must be >= 0");
+  if (o.minIter < 0) fail_arg("minIter must be >= 0");
+  if (o.norm != LDU_NORM_L2 && o.norm != LDU_NORM_OPENFOAM) fail_arg("unknown norm");
+  if (o.batch < 0) fail_arg("batch must be >= 0");
+  if (o.profile != 0 && o.profile != 1) fail_arg("profile must be 0 or 1");
+  const bool profile = o.profile == 1;
+  const int batch = o.batch ? o.batch : 8;
+
+  ensure_amg_work(h, pipelined);
+  const int n = h->n;
+  cudaStream_t s = h->own_stream;
+  h->stats = ldu_solve_stats{};
+  long long kernels = 0;
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, h->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_fork, 0));
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev[0], s));
+  const bool bd = is_device_ptr(b), xd = is_device_ptr(x);
+  const double* bin = b;
+  if (!bd) {
+    ensure_vec(h->bbuf, n);
+    CUDA_CHECK(cudaMemcpyAsync(h->bbuf, b, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    h->stats.h2dBytes += 8LL * n;
+    bin = h->bbuf;
+  }
+  CUDA_CHECK(cudaMemcpyAsync(h->x, x, sizeof(double) * n, xd ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  if (!xd) h->stats.h2dBytes += 8LL * n;
+  if (o.recordHistory && h->histCap < maxIter + 1) {
+    dfree(h->hist);
+    h->hist = nullptr;
+    h->histCap = 0;
+    h->hist = dmalloc<double>((size_t)maxIter + 1);
+    h->histCap = maxIter + 1;
+  }
+  h->histN = -1;
+  State* sh = h->st_host;
+  std::memset(sh, 0, sizeof(State));
+  sh->tol = tol;
+  sh->relTol = o.relTol;
+  sh->minIter = o.minIter;
+  sh->maxIter = maxIter;
+  sh->norm = o.norm;
+  sh->record = o.recordHistory ? 1 : 0;
+  sh->hist = h->hist;
+  sh->histCap = h->histCap;
+  CUDA_CHECK(cudaMemcpyAsync(h->st, sh, sizeof(State), cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaMemsetAsync(h->ticket, 0, 2 * sizeof(unsigned), s));
+  CUDA_CHECK(cudaMemsetAsync(h->p0, 0, sizeof(double) * n, s));
+  if (!pipelined) {
+    CUDA_CHECK(cudaMemsetAsync(h->p1, 0, sizeof(double) * n, s));
+  } else {
+    CUDA_CHECK(cudaMemsetAsync(h->z, 0, sizeof(double) * n, s));
+    CUDA_CHECK(cudaMemsetAsync(h->s, 0, sizeof(double) * n, s));
+    CUDA_CHECK(cudaMemsetAsync(H->qk, 0, sizeof(double) * n, s));
+  }
+
+  // ---- r0 = b - A x0 and the criterion scale ---------------------------------------------
+  double* sumA = pipelined ? h->nv : h->q;
+  if (o.norm == LDU_NORM_OPENFOAM) {
+    k_fill<<<small_grid(n), kBlock, 0, s>>>(n, 1.0, h->r);
+    ++kernels;
+    amul_dev(h, h->r, sumA, s, kernels);
+    k_sum_x<<<h->grid, kBlock, 0, s>>>(n, h->x, h->st, red_of(h, CTL_XBAR, true));
+    ++kernels;
+  }
+  amul_dev(h, h->x, h->ybuf, s, kernels);
+  k_resid<<<h->grid, kBlock, 0, s>>>(n, bin, h->ybuf, sumA, h->rD, h->r, h->st,
+                                     red_of(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, true));
+  ++kernels;
+  if (pipelined) {  // u0 = B r0; w0 = A u0; first fused reduction
+    kernels += enqueue_vcycle(h, h->r, H->u, s, h->st, nullptr);
+    launch_amul(h, H->u, h->w, s);
+    k_amg_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->r, H->u, h->w, h->st, red_of(h, CTL_PIPE_TOP, true));
+    kernels += 2;
+  }
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaEventRecord(h->ev[1], s));
+
+  // ---- iteration batches as CUDA graphs (one per solver; rebuilt with the hierarchy) -------
+  const int gi = (pipelined ? 1 : 0) + (profile ? 2 : 0);
+  if (profile && (int)h->prof_ev.size() < 4 * batch) {
+    for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
+    h->prof_ev.assign(4 * batch, nullptr);
+    for (auto& e : h->prof_ev) CUDA_CHECK(cudaEventCreate(&e));
+    for (int k = 2; k < 4; ++k)
+      if (H->graph[k]) { cudaGraphExecDestroy(H->graph[k]); H->graph[k] = nullptr; }
+    if (h->graphs[0][1].exec) { cudaGraphExecDestroy(h->graphs[0][1].exec); h->graphs[0][1] = {}; }
+    if (h->graphs[1][1].exec) { cudaGraphExecDestroy(h->graphs[1][1].exec); h->graphs[1][1] = {}; }
+  }
+  if (!H->graph[gi] || H->graphBatch[gi] != batch) {
+    if (H->graph[gi]) cudaGraphExecDestroy(H->graph[gi]);
+    H->graph[gi] = nullptr;
+    cudaGraph_t g;
+    CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    H->graphKernels[gi] = enqueue_amg_iters(h, pipelined, batch, s, profile);
+    CUDA_CHECK(cudaStreamEndCapture(s, &g));
+    CUDA_CHECK(cudaGraphInstantiate(&H->graph[gi], g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+    H->graphBatch[gi] = batch;
+  }
+  std::vector<float> passT;
+  int batches = 0;
+  if (maxIter > 0) {
+    for (;;) {
+      CUDA_CHECK(cudaGraphLaunch(H->graph[gi], s));
+      ++batches;
+      if (tol == 0.0 && !profile && o.relTol == 0.0) {  // fixed iterations: sync at the end only
+        if ((long long)batches * batch >= maxIter) break;
+        continue;
+      }
+      CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      if (profile)
+        for (int it = 0; it < batch; ++it)
+          for (int p = 0; p < 2; ++p) {
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, h->prof_ev[4 * it + 2 * p], h->prof_ev[4 * it + 2 * p + 1]));
+            passT.push_back(ms);
+          }
+      if (sh->done) break;
+      if ((long long)batches * batch >= (long long)maxIter + batch) break;  // safety net
+    }
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev[2], s));
+  k_cg_final<<<small_grid(n), kBlock, 0, s>>>(n, h->p0, h->p1, h->x, h->st);
+  ++kernels;
+  CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaMemcpyAsync(x, h->x, sizeof(double) * n, xd ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if (!xd) h->stats.d2hBytes += 8LL * n;
+  CUDA_CHECK(cudaEventRecord(h->ev[3], s));
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+    CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_fork, 0));
+  }
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  CUDA_CHECK(cudaGetLastError());
+  float ms = 0.f;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[3]));
+  h->stats.solveMs = ms;
+  CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]));
+  h->stats.iterMs = ms;
+  h->stats.kernels = kernels + (long long)batches * H->graphKernels[gi];
+  h->stats.allreduces = 0;
+  h->stats.iterations = sh->iter;
+  if (profile)  // pass 0 = V-cycle, pass 1 = Krylov passes, over the iterations that did work
+    for (long long g = 0; g < sh->iter && g < (long long)passT.size() / 2; ++g)
+      for (int p = 0; p < 2; ++p) {
+        h->stats.passMs[p] += passT[2 * g + p];
+        h->stats.passLaunches[p] += 1;
+      }
+  if (sh->record) h->histN = std::min(sh->iter + 1, h->histCap);
+  if (!sh->done) sh->status = LDU_NOT_CONVERGED;
+  if (nIter) *nIter = sh->iter;
+  if (finalRes) *finalRes = sh->res;
+  return (ldu_status)sh->status;
+}
+
+}  // namespace ldu

@@ -5,6 +5,7 @@
 #include <cstring>
 #include <string>
 
+#include "ldu_amg.cuh"
 #include "ldu_impl.cuh"
 
 namespace {
@@ -33,6 +34,7 @@ void destroy_handle(ldu_handle h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
+  ldu::amg_release(h);
   ldu::release_work(h);
   ldu::p2p_release(h);
   for (void* p : {(void*)h->U, (void*)h->slicePtr, (void*)h->npairs, (void*)h->col,
@@ -262,6 +264,68 @@ ldu_status ldu_stream_triad(int device, long long n, int reps, double* gbps) {
     if (!gbps || n < 2 || reps < 1) ldu::fail_arg("bad argument");
     *gbps = ldu::stream_triad(device, n, reps);
     return LDU_OK;
+  });
+}
+
+ldu_status ldu_amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
+  return guard("ldu_amg_setup", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    ldu::amg_setup(h, opts);
+    return LDU_OK;
+  });
+}
+
+ldu_status ldu_amg_get_info(ldu_handle h, ldu_amg_info* out) {
+  return guard("ldu_amg_get_info", [&] {
+    if (!h || !out) ldu::fail_arg("NULL argument");
+    ldu::amg_info(h, out);
+    return LDU_OK;
+  });
+}
+
+ldu_status ldu_amg_get_matrix(ldu_handle h, int level, int which, int* ptr, int* col, double* val) {
+  return guard("ldu_amg_get_matrix", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    ldu::amg_export(h, level, which, ptr, col, val);
+    return LDU_OK;
+  });
+}
+
+ldu_status ldu_amg_get_aggregates(ldu_handle h, int level, int* agg) {
+  return guard("ldu_amg_get_aggregates", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    ldu::amg_export_agg(h, level, agg);
+    return LDU_OK;
+  });
+}
+
+ldu_status ldu_amg_vcycle(ldu_handle h, const double* r, double* z) {
+  return guard("ldu_amg_vcycle", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    ldu::amg_vcycle(h, r, z);
+    return LDU_OK;
+  });
+}
+
+ldu_status amg_pcg_solve(ldu_handle h, const double* b, double* x, double tol, int maxIter,
+                         const ldu_solve_opts* opts, int* nIter, double* finalRes) {
+  return guard("amg_pcg_solve", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    return ldu::amg_solve(h, false, b, x, tol, maxIter, opts, nIter, finalRes);
+  });
+}
+
+ldu_status amg_pipecg_solve(ldu_handle h, const double* b, double* x, double tol, int maxIter,
+                            const ldu_solve_opts* opts, int* nIter, double* finalRes) {
+  return guard("amg_pipecg_solve", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    return ldu::amg_solve(h, true, b, x, tol, maxIter, opts, nIter, finalRes);
   });
 }
 

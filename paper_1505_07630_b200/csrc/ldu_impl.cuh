@@ -113,9 +113,15 @@ struct ldu_comm_s {
   ncclComm_t halo = nullptr;  // halo send / recv
 };
 
+namespace ldu {
+struct AmgHierarchy;  // ldu_amg.cuh
+}
+
 struct ldu_handle_s {
   int device = 0;
   int n = 0, nf = 0;
+  bool symmetric = true;              // lower == NULL or bitwise equal to upper
+  ldu::AmgHierarchy* amg = nullptr;   // aggregation-AMG hierarchy (ldu_amg_setup)
   cudaStream_t own_stream = nullptr, stream = nullptr;
   cudaStream_t red_stream = nullptr, halo_stream = nullptr;
   int layout = 0;

@@ -253,9 +253,28 @@ __device__ __forceinline__ void ctl_pipe_top(State* st, const double* s) {
   st->alpha_old = a;
 }
 
+// AMG-PCG (NEXT-2), after the V-cycle z_k = B r_k: s = [(z_k, r_k)]; beta_0 = 0 (p_0 = z_0)
+__device__ __forceinline__ void ctl_amg_rho(State* st, const double* s) {
+  const double rho = s[0];
+  st->beta = (st->k == 0) ? 0.0 : rho / st->rho;
+  st->rho = rho;
+}
+
+// AMG-PCG, after r_{k+1} = r_k - alpha_k q_k: s = [crit piece(r_{k+1})]
+__device__ __forceinline__ void ctl_amg_B(State* st, const double* s) {
+  const int it = st->k + 1;
+  st->iter = it;
+  st->xpending = 1;  // alpha_k p_k still to be added to x
+  const double res = crit_value(st, s[0]);
+  record(st, it, res);
+  if (converged(st, res, it)) finish(st, LDU_OK, it);
+  else if (it >= st->maxIter) finish(st, LDU_NOT_CONVERGED, it);
+  else st->k = it;
+}
+
 // control selector for the "last block" epilogue of a pass (single rank) or the ctl kernel
 enum Ctl : int { CTL_NONE = 0, CTL_CG_INIT, CTL_PIPE_SCALE, CTL_XBAR, CTL_CG_A, CTL_CG_B,
-                 CTL_PIPE_TOP, CTL_PIPE_NEXT };
+                 CTL_PIPE_TOP, CTL_PIPE_NEXT, CTL_AMG_RHO, CTL_AMG_B };
 
 __device__ __forceinline__ void run_ctl(int ctl, State* st, const double* s) {
   switch (ctl) {
@@ -266,6 +285,8 @@ __device__ __forceinline__ void run_ctl(int ctl, State* st, const double* s) {
     case CTL_CG_B: ctl_cg_B(st, s); break;
     case CTL_PIPE_TOP: ctl_pipe_top(st, s); break;
     case CTL_PIPE_NEXT: st->k += 1; ctl_pipe_top(st, s); break;
+    case CTL_AMG_RHO: ctl_amg_rho(st, s); break;
+    case CTL_AMG_B: ctl_amg_B(st, s); break;
     default: break;
   }
 }

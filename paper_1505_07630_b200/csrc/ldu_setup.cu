@@ -252,6 +252,7 @@ void build_layout(ldu_handle h, const int* l_in, const int* u_in, const double* 
     symmetric = (hf == 0);
     if (symmetric) lo = nullptr;
   }
+  h->symmetric = symmetric;
 
   // ---- banded symmetric => DIA ------------------------------------------------------------
   bool dia = false;

@@ -2015,3 +2015,6 @@ double stream_triad(int device, long long n, int reps) {
 }
 
 }  // namespace ldu
+
+// aggregation-AMG V-cycle and AMG-preconditioned solvers (NEXT-2), same translation unit
+#include "ldu_amg_solve.cuh"
