@@ -27,14 +27,28 @@ struct CsrMat {
   int* col = nullptr;     // [nnz]
   double* val = nullptr;  // [nnz]
   int group = 1;          // lanes per row of the CSR-vector SpMV (power of two <= 32)
+  // optional SELL-32 copy for the V-cycle (coarse A_l with near-uniform rows): 32-row slices,
+  // lane-interleaved (col, val) pairs, padding = (own row, 0.0) so rows need no break test
+  bool useSell = false;
+  long long* slicePtr = nullptr;  // [nslices + 1] in pair rows
+  int* npairs = nullptr;          // [nslices]
+  int2* scol = nullptr;
+  double2* sval = nullptr;
+  long long sellSlots = 0;        // pair slots x 32
   void release() {
-    dfree(ptr);
-    dfree(col);
-    dfree(val);
+    for (void* p : {(void*)ptr, (void*)col, (void*)val, (void*)slicePtr, (void*)npairs,
+                    (void*)scol, (void*)sval})
+      dfree(p);
     ptr = nullptr;
     col = nullptr;
     val = nullptr;
+    slicePtr = nullptr;
+    npairs = nullptr;
+    scol = nullptr;
+    sval = nullptr;
     nnz = 0;
+    sellSlots = 0;
+    useSell = false;
   }
 };
 
@@ -47,6 +61,9 @@ struct CsrView {
 };
 
 inline CsrView view(const CsrMat& m) { return CsrView{m.nrows, m.ptr, m.col, m.val}; }
+inline SellView sell_view(const CsrMat& m) {
+  return SellView{m.nrows, m.slicePtr, m.npairs, m.scol, m.sval};
+}
 
 // One level l < L of the hierarchy: A_l (n x n), aggregates, P_l (n x nc), R_l = P_l^T.
 struct AmgLevel {

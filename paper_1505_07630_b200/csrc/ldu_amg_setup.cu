@@ -75,10 +75,12 @@ void exclusive_scan(const T* in, T* out, long long n, cudaStream_t s) {
   CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws, bytes, tmp, out, n + 1, s));
 }
 
+// lanes per row of the CSR-vector kernels: one trip of kCsrU entries per lane covers an average
+// row (kCsrU = 4 for one lane per row, 8 otherwise; ldu_amg_solve.cuh)
 int group_of(long long nnz, int rows) {
   const double avg = rows ? (double)nnz / rows : 1.0;
   int g = 1;
-  while (g < 32 && g < avg) g <<= 1;
+  while (g < 32 && (g == 1 ? 4.0 : 8.0 * g) < avg) g <<= 1;
   return g;
 }
 
@@ -575,6 +577,61 @@ double lanczos_omega(const CsrMat& A, const double* diag, int steps, cudaStream_
 }
 
 // ---------------------------------------------------------------------------------------------
+// SELL-32 copy of a CSR for the V-cycle (coarse A_l): slice width = longest row of 32
+// ---------------------------------------------------------------------------------------------
+__global__ void k_sell_width(int n, const int* __restrict__ ptr, long long* __restrict__ np) {
+  GSTRIDE(sl, (n + 31) / 32) {
+    int w = 0;
+    for (int r = (int)sl * 32; r < min(n, (int)sl * 32 + 32); ++r) w = max(w, ptr[r + 1] - ptr[r]);
+    np[sl] = (w + 1) / 2;
+  }
+}
+__global__ void k_l2i_n(long long n, const long long* __restrict__ a, int* __restrict__ b) {
+  GSTRIDE(i, n) b[i] = (int)a[i];
+}
+__global__ void k_sell_fill(CsrView A, const long long* __restrict__ sp, const int* __restrict__ np,
+                            int* __restrict__ col, double* __restrict__ val) {
+  GSTRIDE(r, A.n) {
+    const long long sl = r >> 5, lane = r & 31;
+    const int b = A.ptr[r], e = A.ptr[r + 1];
+    for (int jj = 0; jj < np[sl]; ++jj) {
+      const long long slot = ((sp[sl] + jj) * 32 + lane) * 2;
+      for (int h = 0; h < 2; ++h) {
+        const int k = b + 2 * jj + h;
+        col[slot + h] = k < e ? A.col[k] : (int)r;  // padding: own row, coefficient 0
+        val[slot + h] = k < e ? A.val[k] : 0.0;
+      }
+    }
+  }
+}
+
+// Attach a SELL-32 copy when its padded slots stay within maxPad x the CSR entries.
+void attach_sell(CsrMat& M, double maxPad, cudaStream_t s) {
+  // one row per thread needs enough rows to fill the GPU; small levels stay CSR-vector
+  if (M.nrows < 65536 || M.nnz <= 0) return;
+  Scratch sc;
+  const long long ns = (M.nrows + 31) / 32;
+  long long* np = sc.get<long long>(ns + 1);
+  long long* sp = dmalloc<long long>(ns + 1);
+  k_sell_width<<<nblk(ns), kSB, 0, s>>>(M.nrows, M.ptr, np);
+  exclusive_scan<long long>(np, sp, ns, s);
+  const long long pairs = d2h(sp + ns, s);
+  if ((double)pairs * 64.0 > maxPad * (double)M.nnz) {
+    dfree(sp);
+    return;
+  }
+  M.slicePtr = sp;
+  M.npairs = dmalloc<int>(ns);
+  k_l2i_n<<<nblk(ns), kSB, 0, s>>>(ns, np, M.npairs);
+  M.sellSlots = pairs * 32;
+  M.scol = dmalloc<int2>(M.sellSlots);
+  M.sval = dmalloc<double2>(M.sellSlots);
+  k_sell_fill<<<nblk(M.nrows), kSB, 0, s>>>(view(M), sp, M.npairs, (int*)M.scol, (double*)M.sval);
+  CUDA_CHECK(cudaGetLastError());
+  M.useSell = true;
+}
+
+// ---------------------------------------------------------------------------------------------
 // prolongator, restriction, Galerkin product
 // ---------------------------------------------------------------------------------------------
 __global__ void k_diag_of(CsrView A, double* __restrict__ diag, double* __restrict__ rD,
@@ -943,6 +1000,9 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
         L.f = dmalloc<double>(n);
         L.z = dmalloc<double>(n);
       }
+      attach_sell(L.R, 1.25, s);  // V-cycle copies where rows are near-uniform
+      attach_sell(L.P, 1.25, s);
+      attach_sell(Ac, 1.25, s);
       H->lv.push_back(L);
       // next level's diagonal
       diag = dmalloc<double>(Ac.nrows);
@@ -1009,7 +1069,8 @@ void amg_info(ldu_handle h, ldu_amg_info* out) {
     out->omega[l] = L.omega;
     tot += L.A.nnz;
     bytes += 12LL * (L.A.nnz + L.P.nnz + L.R.nnz) + 4LL * (2 * L.n + L.nc + 3) + 8LL * 2 * L.n +
-             4LL * L.n + (l ? 8LL * 4 * L.n : 0);
+             4LL * L.n + (l ? 8LL * 4 * L.n : 0) +
+             12LL * (L.A.sellSlots + L.P.sellSlots + L.R.sellSlots);
   }
   out->n[H->L] = H->nc;
   out->nnzA[H->L] = H->Ac.nnz;

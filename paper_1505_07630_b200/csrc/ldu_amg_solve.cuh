@@ -30,9 +30,13 @@ namespace ldu {
 namespace {
 
 // ---- CSR-vector rows: `G` lanes per row, grid-stride over warps -------------------------------
+// Each lane sums the entries k = start + sub, + G, + 2G, ... of its row in that order (U of them
+// per trip, loads issued together for memory-level parallelism), then the G lanes combine in a
+// fixed xor-butterfly: deterministic.  G is chosen per matrix so that a lane holds ~U entries.
 template <int G, class Epi>
 __global__ void __launch_bounds__(kBlock) k_csr_vec(CsrView A, Epi e, const State* st) {
   if (st && st->done) return;
+  constexpr int kCsrU = G == 1 ? 4 : 8;  // entries per lane per trip (see group_of)
   constexpr int RPW = 32 / G;  // rows per warp
   const int lane = threadIdx.x & 31, sub = lane & (G - 1);
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -42,8 +46,22 @@ __global__ void __launch_bounds__(kBlock) k_csr_vec(CsrView A, Epi e, const Stat
     double s = 0.0;
     if (row < A.n) {
       const int end = __ldg(A.ptr + row + 1);
-      for (int k = __ldg(A.ptr + row) + sub; k < end; k += G)
-        s = fma(__ldg(A.val + k), e.in(__ldg(A.col + k)), s);
+      for (int k = __ldg(A.ptr + row) + sub; k < end; k += kCsrU * G) {
+        int c[kCsrU];
+        double v[kCsrU], x[kCsrU];
+#pragma unroll
+        for (int u = 0; u < kCsrU; ++u) {
+          const int kk = k + u * G;
+          const bool ok = kk < end;
+          c[u] = ok ? __ldg(A.col + kk) : 0;
+          v[u] = ok ? __ldg(A.val + kk) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kCsrU; ++u) x[u] = e.in(c[u]);
+#pragma unroll
+        for (int u = 0; u < kCsrU; ++u)
+          if (k + u * G < end) s = fma(v[u], x[u], s);
+      }
     }
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -51,21 +69,26 @@ __global__ void __launch_bounds__(kBlock) k_csr_vec(CsrView A, Epi e, const Stat
   }
 }
 
-struct EpiPre {  // K1: r = f - A (w rD f)
-  double w;
-  const double* __restrict__ rD;
+struct EpiPre {  // K1 at level >= 1: r = f - A xpre, xpre = w rD f stored by the restriction
+  const double* __restrict__ xpre;
   const double* __restrict__ f;
   double* __restrict__ r;
-  __device__ __forceinline__ double in(int j) const { return w * __ldg(rD + j) * __ldg(f + j); }
+  __device__ __forceinline__ double in(int j) const { return __ldg(xpre + j); }
   __device__ __forceinline__ void out(int i, double s) const { r[i] = f[i] - s; }
 };
-struct EpiCopy {  // K2: y = M x
-  const double* __restrict__ x;
-  double* __restrict__ y;
-  __device__ __forceinline__ double in(int j) const { return __ldg(x + j); }
-  __device__ __forceinline__ void out(int i, double s) const { y[i] = s; }
+struct EpiRestrict {  // K2: f_c = R r; and the next level's pre-sweep iterate w_c rD_c f_c
+  const double* __restrict__ r;
+  double* __restrict__ fc;
+  double* __restrict__ xpre;  // nullptr for the coarsest level
+  double w;
+  const double* __restrict__ rDc;
+  __device__ __forceinline__ double in(int j) const { return __ldg(r + j); }
+  __device__ __forceinline__ void out(int i, double s) const {
+    fc[i] = s;
+    if (xpre) xpre[i] = w * rDc[i] * s;
+  }
 };
-struct EpiProlong {  // K3: x = w rD f + P xc
+struct EpiProlong0 {  // K3 at level 0: x = w rD f + P xc
   double w;
   const double* __restrict__ rD;
   const double* __restrict__ f;
@@ -73,6 +96,12 @@ struct EpiProlong {  // K3: x = w rD f + P xc
   double* __restrict__ x;
   __device__ __forceinline__ double in(int j) const { return __ldg(xc + j); }
   __device__ __forceinline__ void out(int i, double s) const { x[i] = w * rD[i] * f[i] + s; }
+};
+struct EpiProlong {  // K3 at level >= 1: x = xpre + P xc (in place over xpre)
+  const double* __restrict__ xc;
+  double* x;
+  __device__ __forceinline__ double in(int j) const { return __ldg(xc + j); }
+  __device__ __forceinline__ void out(int i, double s) const { x[i] = x[i] + s; }
 };
 struct EpiPost {  // K4: z = x + w rD (f - A x)
   double w;
@@ -84,6 +113,49 @@ struct EpiPost {  // K4: z = x + w rD (f - A x)
   __device__ __forceinline__ void out(int i, double s) const { z[i] = x[i] + w * rD[i] * (f[i] - s); }
 };
 
+// SELL-32 rows (coarse A_l, see attach_sell): one row per thread, lane-interleaved pairs, 4 pair
+// loads in flight per trip; padding is (own row, 0) so there is no data-dependent exit
+template <class Epi>
+__global__ void __launch_bounds__(kBlock) k_sell_rows(SellView A, Epi e, const State* st) {
+  if (st && st->done) return;
+  GRID_STRIDE(c, A.n) {
+    const int slice = c >> 5, lane = c & 31;
+    const long long base = __ldg(A.slicePtr + slice);
+    const int np = __ldg(A.npairs + slice);
+    double s = 0.0;
+    int jj = 0;
+    for (; jj + 4 <= np; jj += 4) {
+      int2 cc[4];
+      double2 vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long q = (base + jj + u) * 32 + lane;
+        cc[u] = __ldg(A.col + q);
+        vv[u] = __ldg(A.val + q);
+      }
+      double x0[4], x1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x0[u] = e.in(cc[u].x);
+        x1[u] = e.in(cc[u].y);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s = fma(vv[u].x, x0[u], s);
+        s = fma(vv[u].y, x1[u], s);
+      }
+    }
+    for (; jj < np; ++jj) {
+      const long long q = (base + jj) * 32 + lane;
+      const int2 cc = __ldg(A.col + q);
+      const double2 vv = __ldg(A.val + q);
+      s = fma(vv.x, e.in(cc.x), s);
+      s = fma(vv.y, e.in(cc.y), s);
+    }
+    e.out(c, s);
+  }
+}
+
 int csr_grid(long long rows, int G) {
   const long long warps = (rows + 32 / G - 1) / (32 / G);
   const long long b = (warps * 32 + kBlock - 1) / kBlock;
@@ -92,6 +164,11 @@ int csr_grid(long long rows, int G) {
 
 template <class Epi>
 void launch_csr(const CsrMat& M, const Epi& e, const State* st, cudaStream_t s) {
+  if (M.useSell) {
+    const long long b = ((long long)M.nrows + kBlock - 1) / kBlock;
+    k_sell_rows<<<(int)std::max(1LL, std::min(b, 148LL * 8)), kBlock, 0, s>>>(sell_view(M), e, st);
+    return;
+  }
   const CsrView v = view(M);
   const int g = csr_grid(M.nrows, M.group);
   switch (M.group) {
@@ -271,10 +348,14 @@ long long enqueue_vcycle(ldu_handle h, const double* f0, double* z0, cudaStream_
         k_vc_pre<<<h->gridA, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f, Lv.r, st);
       });
     } else {
-      launch_csr(Lv.A, EpiPre{Lv.omega, Lv.rD, f, Lv.r}, st, s);
+      launch_csr(Lv.A, EpiPre{Lv.x, f, Lv.r}, st, s);
     }
-    double* fc = (l + 1 == L) ? H->fL : H->lv[l + 1].f;
-    launch_csr(Lv.R, EpiCopy{Lv.r, fc}, st, s);
+    if (l + 1 < L) {
+      AmgLevel& Nx = H->lv[l + 1];
+      launch_csr(Lv.R, EpiRestrict{Lv.r, Nx.f, Nx.x, Nx.omega, Nx.rD}, st, s);
+    } else {
+      launch_csr(Lv.R, EpiRestrict{Lv.r, H->fL, nullptr, 0.0, nullptr}, st, s);
+    }
     kernels += 2;
   }
   {
@@ -292,8 +373,8 @@ long long enqueue_vcycle(ldu_handle h, const double* f0, double* z0, cudaStream_
     AmgLevel& Lv = H->lv[l];
     const double* f = l ? Lv.f : f0;
     const double* xc = (l + 1 == L) ? H->zL : H->lv[l + 1].z;
-    launch_csr(Lv.P, EpiProlong{Lv.omega, Lv.rD, f, xc, Lv.x}, st, s);
     if (l == 0) {
+      launch_csr(Lv.P, EpiProlong0{Lv.omega, Lv.rD, f, xc, Lv.x}, st, s);
       with_format(h, [&](auto A) {
         if (rho)
           k_vc_post<decltype(A), true><<<h->gridA, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f,
@@ -303,6 +384,7 @@ long long enqueue_vcycle(ldu_handle h, const double* f0, double* z0, cudaStream_
                                                                     Lv.x, z0, st, Red{});
       });
     } else {
+      launch_csr(Lv.P, EpiProlong{xc, Lv.x}, st, s);
       launch_csr(Lv.A, EpiPost{Lv.omega, Lv.rD, f, Lv.x, Lv.z}, st, s);
     }
     kernels += 2;

@@ -1683,7 +1683,9 @@ void p2p_setup(ldu_handle h) {
     throw Error(LDU_ERR_INVALID_ARG, "peer-memory path supports <= 64 ranks and <= 16 interfaces");
   cudaStream_t s = h->own_stream;
   const size_t bytes = MailboxLayout::bytes(h->nIfFaces);
-  h->mailbox = dmalloc<char>(bytes);
+  // a plain (never staggered) allocation: peers map it through its CUDA IPC handle, which
+  // names the allocation base
+  CUDA_CHECK(cudaMalloc((void**)&h->mailbox, bytes));
   CUDA_CHECK(cudaMemset(h->mailbox, 0, bytes));
   // interface index of every packed face
   std::vector<int> faceIf(std::max(1, h->nIfFaces), 0);

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--jacobi", type=int, default=1)
+    ap.add_argument("--only", default="", help="comma-separated solver names")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for n in a.n:
@@ -39,6 +40,8 @@ def main():
             solvers = [("amg_pcg", A.amg_pcg_solve), ("amg_pipecg", A.amg_pipecg_solve)]
             if a.jacobi:
                 solvers += [("jacobi_pcg", A.pcg_solve), ("jacobi_pipecg", A.pipecg_solve)]
+            if a.only:
+                solvers = [sv for sv in solvers if sv[0] in a.only.split(",")]
             for name, fn in solvers:
                 ms, its = [], []
                 for r in range(a.reps + 1):
