@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="skip per-pass event timing")
+    p.add_argument("--no-amg", action="store_true", help="skip the AMG-PCG time-to-solution leg")
+    p.add_argument("--amg-tol", type=float, default=1e-8)
     return p.parse_args()
 
 
@@ -84,6 +86,26 @@ def pass_format_bytes(solver, info, N):
         return 56 * N + 8 * info["nDiagonals"] * N  # r, rD, p_old, x in; p, q, x out; U_k once
     base = 48 * N + 24 * N if split else 56 * N
     return base + 12 * info["storedEntries"] + 12 * ((N + 31) // 32)
+
+
+def vcycle_bytes(amg, info):
+    """Bytes one V-cycle must move in the layouts it streams: level 0 on the
+    handle's DIA layout (nd coefficient arrays), coarser levels and every P / R as CSR (12 B per
+    entry + 4 B row pointer), each vector touched once per kernel, the coarsest dense inverse."""
+    n, nA, nP, L = amg["n"], amg["nnzA"], amg["nnzP"], amg["nLevels"]
+    tot = 0
+    for l in range(L):
+        N, Nc = n[l], n[l + 1]
+        if l == 0 and info["layout_name"] == "DIA_SYM":
+            a = 8 * info["nDiagonals"] * N + 8 * N        # U_k and diag
+        else:
+            a = 12 * nA[l] + 4 * N
+        tot += a + 8 * N + 16 * N                         # K1: A, x_pre (gathered), f in, r out
+        tot += 12 * nP[l] + 4 * Nc + 8 * N + 16 * Nc      # K2: R, r in; f_c, x_pre,c out
+        tot += 12 * nP[l] + 4 * N + 8 * Nc + (24 if l == 0 else 16) * N  # K3: P, x_c (+ rD, f) in; x
+        tot += a + 8 * N + 24 * N                         # K4: A, x, f, rD in; z out
+    nc = amg["coarsestN"]
+    return tot + 8 * nc * nc + 16 * nc
 
 
 def hbm_peak():
@@ -395,6 +417,56 @@ def main():
         e2e = {"value": args.steps * args.iters / float(te.item()), "unit": UNIT,
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
 
+    # AMG-PCG (NEXT-2): time to solution at --amg-tol vs Jacobi-PCG on the same system
+    amg = None
+    if world == 1 and not args.no_amg:
+        ai = A.amg_setup()
+        tol = args.amg_tol
+        for _ in range(2):
+            x.zero_()
+            A.amg_pcg_solve(b, x, tol=tol, maxIter=1000)
+        barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        akern = 0
+        for _ in range(args.steps):
+            x.zero_()
+            ast, ait, ares = A.amg_pcg_solve(b, x, tol=tol, maxIter=1000)
+            akern += A.stats()["kernels"]
+        a1.record(stream)
+        barrier()
+        t_amg = a0.elapsed_time(a1) / 1e3 / args.steps
+        x.zero_()
+        A.amg_pcg_solve(b, x, tol=tol, maxIter=1000, profile=True)
+        ps = A.stats()
+        vc_ms = ps["passMs"][0] / max(1, ps["passLaunches"][0])
+        kr_ms = ps["passMs"][1] / max(1, ps["passLaunches"][1])
+        x.zero_()
+        A.pcg_solve(b, x, tol=tol, maxIter=20000)
+        barrier()
+        j0 = torch.cuda.Event(enable_timing=True)
+        j1 = torch.cuda.Event(enable_timing=True)
+        j0.record(stream)
+        x.zero_()
+        jst, jit, jres = A.pcg_solve(b, x, tol=tol, maxIter=20000)
+        j1.record(stream)
+        barrier()
+        t_jac = j0.elapsed_time(j1) / 1e3
+        vb = vcycle_bytes(ai, info)
+        amg = {"solver": "amg_pcg (smoothed-aggregation AMG V-cycle, Jacobi w-smoother; P:236)",
+               "tol": tol, "status": int(ast), "iterations": ait, "final_res": ares,
+               "ms_per_solve": 1e3 * t_amg, "ms_per_iter": 1e3 * t_amg / max(1, ait),
+               "setup_ms": ai["setupMs"], "levels": ai["n"],
+               "operator_complexity": ai["operatorComplexity"],
+               "jacobi_pcg": {"iterations": jit, "ms_per_solve": 1e3 * t_jac, "status": int(jst)},
+               "time_to_solution_speedup_vs_jacobi_pcg": t_jac / t_amg,
+               "gpu_launches_per_solve": akern // args.steps,
+               "vcycle": {"ms": vc_ms, "krylov_passes_ms": kr_ms, "bytes": vb,
+                          "achieved": vb / (vc_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                          "frac": vb / (vc_ms / 1e3) / 1e9 / peak, "bound": "hbm",
+                          "peak_source": peak_src}}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         k1, k2 = 3, 15
@@ -414,7 +486,7 @@ def main():
                "effective_frac_of_hbm": value * bytes_iter / 1e9 / (peak * world),
                "bytes_per_iter_model": bytes_iter,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels,
-               "secondary": secondary,
+               "secondary": secondary, "amg": amg,
                "clocks": clk, "last_status": int(st), "iterations_per_step": it}
         print(json.dumps(out), flush=True)
     A.close()

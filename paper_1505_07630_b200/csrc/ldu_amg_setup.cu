@@ -20,6 +20,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "ldu_amg.cuh"
@@ -41,16 +44,27 @@ int nblk(long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)(n); \
        i += (long long)gridDim.x * blockDim.x)
 
-struct Scratch {  // frees every registered allocation on scope exit
+// Stream-ordered scratch from the device's memory pool (cudaMallocAsync): the setup allocates
+// and frees tens of GB of temporaries level after level; plain cudaMalloc / cudaFree map and
+// unmap them every time (synchronous, and measured to vary 10x from run to run).  amg_setup
+// keeps the pool's memory until the hierarchy is built, then trims it.
+struct Scratch {
+  cudaStream_t s;
   std::vector<void*> p;
+  explicit Scratch(cudaStream_t st) : s(st) {}
   template <class T>
   T* get(size_t n) {
-    T* q = dmalloc<T>(n);
+    void* q = nullptr;
+    const size_t bytes = std::max<size_t>(1, n) * sizeof(T);
+    if (cudaMallocAsync(&q, bytes, s) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(LDU_ERR_OOM, "cudaMallocAsync of " + std::to_string(bytes) + " bytes failed");
+    }
     p.push_back(q);
-    return q;
+    return static_cast<T*>(q);
   }
   ~Scratch() {
-    for (void* q : p) dfree(q);
+    for (void* q : p) cudaFreeAsync(q, s);
   }
 };
 
@@ -65,7 +79,7 @@ T d2h(const T* d, cudaStream_t s) {
 // exclusive scan of in[0..n) into out[0..n] (out[n] = total)
 template <class T>
 void exclusive_scan(const T* in, T* out, long long n, cudaStream_t s) {
-  Scratch sc;
+  Scratch sc(s);
   T* tmp = sc.get<T>(n + 1);
   CUDA_CHECK(cudaMemsetAsync(tmp + n, 0, sizeof(T), s));
   if (n) CUDA_CHECK(cudaMemcpyAsync(tmp, in, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
@@ -126,7 +140,7 @@ int bits_for(unsigned long long v) {
 // keys / vals [m] are consumed (clobbered).
 CsrMat assemble(int nrows, int ncols, long long m, unsigned long long* keys, double* vals,
                 bool drop, cudaStream_t s) {
-  Scratch sc;
+  Scratch sc(s);
   CsrMat out;
   out.nrows = nrows;
   out.ncols = ncols;
@@ -261,7 +275,7 @@ void with_layout(ldu_handle h, F&& f) {
 }
 
 CsrMat level0_csr(ldu_handle h, cudaStream_t s) {
-  Scratch sc;
+  Scratch sc(s);
   const int n = h->n;
   long long* cnt = sc.get<long long>(n + 1);
   long long* off = sc.get<long long>(n + 1);
@@ -377,8 +391,10 @@ __global__ void k_agg_step4(int n, const int* __restrict__ ptr, const int* __res
   }
 }
 
+int g_mis_rounds = 0;  // rounds of the last aggregation (LDU_AMG_TRACE)
+
 int mis2_aggregate(const CsrMat& A, int hashed, int* agg, cudaStream_t s) {
-  Scratch sc;
+  Scratch sc(s);
   const int n = A.nrows;
   unsigned char* und = sc.get<unsigned char>(n);
   unsigned char* root = sc.get<unsigned char>(n);
@@ -397,6 +413,7 @@ int mis2_aggregate(const CsrMat& A, int hashed, int* agg, cudaStream_t s) {
     CUDA_CHECK(cudaMemsetAsync(left, 0, sizeof(int), s));
     k_mis_retire<<<nblk(n), kSB, 0, s>>>(n, d2, und, left);
     CUDA_CHECK(cudaGetLastError());
+    g_mis_rounds = round + 1;
     if (d2h(left, s) == 0) break;
   }
   int* rf = sc.get<int>(n + 1);
@@ -534,7 +551,7 @@ __global__ void k_tridiag_max(int m, const double* __restrict__ al, const double
 
 double lanczos_omega(const CsrMat& A, const double* diag, int steps, cudaStream_t s,
                      double* ritzOut) {
-  Scratch sc;
+  Scratch sc(s);
   const int n = A.nrows;
   const int G = nblk(n);
   double* v = sc.get<double>(n);
@@ -609,7 +626,7 @@ __global__ void k_sell_fill(CsrView A, const long long* __restrict__ sp, const i
 void attach_sell(CsrMat& M, double maxPad, cudaStream_t s) {
   // one row per thread needs enough rows to fill the GPU; small levels stay CSR-vector
   if (M.nrows < 65536 || M.nnz <= 0) return;
-  Scratch sc;
+  Scratch sc(s);
   const long long ns = (M.nrows + 31) / 32;
   long long* np = sc.get<long long>(ns + 1);
   long long* sp = dmalloc<long long>(ns + 1);
@@ -706,7 +723,7 @@ __global__ void k_l2i(long long n, const long long* __restrict__ a, int* __restr
 }
 
 void drop_zeros(CsrMat& A, cudaStream_t s) {
-  Scratch sc;
+  Scratch sc(s);
   long long* cnt = sc.get<long long>(A.nrows + 1);
   long long* off = sc.get<long long>(A.nrows + 1);
   k_nz_count<<<nblk(A.nrows), kSB, 0, s>>>(view(A), cnt);
@@ -787,7 +804,7 @@ __global__ void k_expand_PtAP(CsrView P, CsrView Q, int nc, const long long* __r
 
 CsrMat build_P(const CsrMat& A, const int* agg, int nAgg, const double* diag, double omega,
                bool smooth, cudaStream_t s) {
-  Scratch sc;
+  Scratch sc(s);
   const int n = A.nrows;
   if (!smooth) {
     unsigned long long* key = sc.get<unsigned long long>(n);
@@ -808,7 +825,7 @@ CsrMat build_P(const CsrMat& A, const int* agg, int nAgg, const double* diag, do
 }
 
 CsrMat transpose(const CsrMat& P, cudaStream_t s) {
-  Scratch sc;
+  Scratch sc(s);
   unsigned long long* key = sc.get<unsigned long long>(P.nnz);
   double* val = sc.get<double>(P.nnz);
   k_expand_T_of<<<nblk(P.nrows), kSB, 0, s>>>(view(P), P.ncols, key, val);
@@ -819,7 +836,7 @@ CsrMat galerkin(const CsrMat& A, const CsrMat& P, cudaStream_t s) {
   const int n = A.nrows, nc = P.ncols;
   CsrMat AP;
   {
-    Scratch sc;
+    Scratch sc(s);
     long long* cnt = sc.get<long long>(n + 1);
     long long* off = sc.get<long long>(n + 1);
     k_count_AP<<<nblk(n), kSB, 0, s>>>(view(A), P.ptr, cnt);
@@ -832,7 +849,7 @@ CsrMat galerkin(const CsrMat& A, const CsrMat& P, cudaStream_t s) {
   }
   CsrMat Ac;
   {
-    Scratch sc;
+    Scratch sc(s);
     long long* cnt = sc.get<long long>(n + 1);
     long long* off = sc.get<long long>(n + 1);
     k_count_PtAP<<<nblk(n), kSB, 0, s>>>(n, P.ptr, AP.ptr, cnt);
@@ -890,7 +907,7 @@ __global__ void k_gj_elim(int n, int k, double* __restrict__ D, double* __restri
 }
 
 double* dense_inverse(const CsrMat& A, cudaStream_t s) {
-  Scratch sc;
+  Scratch sc(s);
   const int n = A.nrows;
   double* D = sc.get<double>((size_t)n * n);
   double* I = dmalloc<double>((size_t)n * n);
@@ -910,6 +927,29 @@ double* dense_inverse(const CsrMat& A, cudaStream_t s) {
   }
   return I;
 }
+
+// LDU_AMG_TRACE=1: per-phase host wall times of the setup on stderr (stream synchronised)
+struct PhaseTrace {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  double t0 = 0;
+  static double now() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
+  PhaseTrace(cudaStream_t st) : s(st) {
+    const char* e = std::getenv("LDU_AMG_TRACE");
+    on = e && std::atoi(e) != 0;
+    t0 = now();
+  }
+  void mark(const char* what, int level) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double t = now();
+    fprintf(stderr, "[ldu amg setup] level %d %-10s %8.2f ms (mis rounds %d)\n", level, what,
+            t - t0, g_mis_rounds);
+    t0 = t;
+  }
+};
 
 void free_level(AmgLevel& L) {
   L.A.release();
@@ -960,6 +1000,10 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
     throw Error(LDU_ERR_STATE, "AMG on multi-rank handles is not supported yet (reading Z33)");
   amg_release(h);
   cudaStream_t s = h->own_stream;
+  cudaMemPool_t pool;
+  CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, h->device));
+  unsigned long long keep = ~0ULL;  // keep freed scratch mapped for reuse during the build
+  CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   if (h->stream != h->own_stream) {
     CUDA_CHECK(cudaEventRecord(h->ev_fork, h->stream));
     CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_fork, 0));
@@ -970,7 +1014,9 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
   h->amg = H;
   try {
     const int hashed = o.keyIndexOrder ? 0 : 1;
+    PhaseTrace tr(s);
     CsrMat A = level0_csr(h, s);
+    tr.mark("csr0", 0);
     double* diag = h->diag;
     double* rD = h->rD;
     bool owns = false;
@@ -978,6 +1024,7 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
       const int n = A.nrows;
       int* agg = dmalloc<int>(n);
       const int nAgg = mis2_aggregate(A, hashed, agg, s);
+      tr.mark("mis2", (int)H->lv.size());
       if (nAgg >= n) {  // no coarsening possible (Z31)
         dfree(agg);
         break;
@@ -991,9 +1038,12 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
       L.ownsDiag = owns;
       L.agg = agg;
       L.omega = lanczos_omega(A, diag, o.lanczosSteps, s, nullptr);
+      tr.mark("lanczos", (int)H->lv.size());
       L.P = build_P(A, agg, nAgg, diag, L.omega, !o.unsmoothed, s);
       L.R = transpose(L.P, s);
+      tr.mark("P,R", (int)H->lv.size());
       CsrMat Ac = galerkin(A, L.P, s);
+      tr.mark("galerkin", (int)H->lv.size());
       L.r = dmalloc<double>(n);
       L.x = dmalloc<double>(n);
       if (!H->lv.empty()) {
@@ -1003,13 +1053,14 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
       attach_sell(L.R, 1.25, s);  // V-cycle copies where rows are near-uniform
       attach_sell(L.P, 1.25, s);
       attach_sell(Ac, 1.25, s);
+      tr.mark("sell", (int)H->lv.size());
       H->lv.push_back(L);
       // next level's diagonal
       diag = dmalloc<double>(Ac.nrows);
       rD = dmalloc<double>(Ac.nrows);
       owns = true;
       {
-        Scratch sc;
+        Scratch sc(s);
         int* bad = sc.get<int>(1);
         CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), s));
         k_diag_of<<<nblk(Ac.nrows), kSB, 0, s>>>(view(Ac), diag, rD, bad);
@@ -1034,6 +1085,7 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
       fail_arg("AMG: coarsest level has " + std::to_string(H->nc) + " rows (> 8192 for the dense solve)");
     }
     H->Ainv = dense_inverse(A, s);
+    tr.mark("inverse", H->L);
     H->Ac = A;  // level L (for L == 0 this is the level-0 CSR itself)
     if (owns) {
       dfree(diag);
@@ -1048,7 +1100,10 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
     float ms = 0.f;
     CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
     H->setupMs = ms;
+    CUDA_CHECK(cudaMemPoolTrimTo(pool, 0));  // return the scratch to the device
   } catch (...) {
+    cudaStreamSynchronize(s);
+    cudaMemPoolTrimTo(pool, 0);
     amg_release(h);
     throw;
   }
