@@ -211,7 +211,8 @@ ldu_status ldu_stream_triad(int device, long long n, int reps, double *gbps);
  *   - coarsening while n > coarsest, the level shrinks and fewer than maxLevels levels exist; the
  *     coarsest system is solved exactly through its dense inverse (Z31; at most 8192 rows);
  *   - multi-rank handles: the hierarchy is built from the rank's local matrix (interfaces
- *     dropped, block-Jacobi across ranks; Z33).  Not supported yet: returns LDU_ERR_STATE.
+ *     dropped), i.e. a block-Jacobi preconditioner across ranks; the Krylov operator keeps the
+ *     interfaces (Z33).  ldu_amg_setup is then local (not collective); the solves are collective.
  * The matrix must be symmetric (lower == NULL or lower == upper); diag > 0.                     */
 typedef struct {
   int coarsest;        /* stop coarsening at n <= coarsest; 0 = 64 (reading Z31)                 */
@@ -238,7 +239,7 @@ typedef struct {
 
 /* Builds the hierarchy on the device for handle h (replacing any previous one).  opts NULL =>
  * defaults.  Errors: INVALID_ARG (bad option, non-symmetric matrix, coarsest level > 8192 rows),
- * STATE (multi-rank handle; a non-positive pivot in the coarsest inverse), CUDA, OOM. */
+ * STATE (a non-positive pivot in the coarsest inverse), CUDA, OOM. */
 ldu_status ldu_amg_setup(ldu_handle h, const ldu_amg_opts *opts);
 ldu_status ldu_amg_get_info(ldu_handle h, ldu_amg_info *out);
 
@@ -252,10 +253,11 @@ ldu_status ldu_amg_get_aggregates(ldu_handle h, int level, int *agg);
 /* z = B r: one V-cycle of the hierarchy (reading Z32).  r, z: [nCells] host or device. */
 ldu_status ldu_amg_vcycle(ldu_handle h, const double *r, double *z);
 
-/* AMG-preconditioned classical CG (SURVEY §8(c) c2 with z = B r; 2 reductions per iteration
- * plus the V-cycle) and pipelined CG (c3 literal Ghysels-Vanroose form with u = B r, m = B w; one
- * fused reduction per iteration).  Same arguments, options and semantics as pcg_solve_ex;
- * STATE if ldu_amg_setup has not been called. */
+/* AMG-preconditioned classical CG (SURVEY §8(c) c2 with z = B r; 3 global reductions per
+ * iteration: (z, r), (p, Ap), crit(r)) and pipelined CG (c3 literal Ghysels-Vanroose form with
+ * u = B r, m = B w; ONE fused reduction per iteration, overlapped across ranks with the V-cycle
+ * and the SpMV of the next iteration).  Same arguments, options and semantics as
+ * pcg_solve_ex; collective on multi-rank handles; STATE if ldu_amg_setup has not been called. */
 ldu_status amg_pcg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,
                          const ldu_solve_opts *opts, int *nIter, double *finalRes);
 ldu_status amg_pipecg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,

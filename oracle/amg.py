@@ -65,6 +65,11 @@ def _lib():
         lib.oracle_amg_vcycle.restype = None
         lib.oracle_amg_pcg.argtypes = [I, I, P, P, P, P, P, P, P, D, I, I, P, P, P, D, I, P, I]
         lib.oracle_amg_pcg.restype = I
+        lib.oracle_amg_block_vcycle.argtypes = [I, I, P, P, P, P]
+        lib.oracle_amg_block_vcycle.restype = I
+        lib.oracle_amg_block_pcg.argtypes = [I, I, P, P, P, P, P, P, P, D, I, I, P, P, P, D, I, I,
+                                             P, P, I]
+        lib.oracle_amg_block_pcg.restype = I
         lib._amg_ready = True
     return lib
 
@@ -272,3 +277,54 @@ def amg_solve(sys, b: np.ndarray, H: Optional[Hierarchy] = None, x0: Optional[np
     if history:
         return st, x, it.value, res.value, hist[: it.value + 1]
     return st, x, it.value, res.value
+
+
+# ---- block-Jacobi AMG across ranks (reading Z33) -------------------------------------------
+def block_hierarchies(parts, **build_kw) -> List[Hierarchy]:
+    """One hierarchy per rank, each from the rank's LOCAL matrix (its own faces only; the
+    interface couplings are dropped) -- ``parts`` as from meshgen.slab_partition."""
+    return [build_hierarchy(csr_of_ldu(p), **build_kw) for p in parts]
+
+
+def _blocks(Hs, bounds):
+    flats = [_flatten(H) for H in Hs]
+    arr = (ctypes.c_void_p * len(flats))(*[ctypes.addressof(f) for f in flats])
+    start = np.ascontiguousarray(bounds, dtype=np.int32)
+    return flats, arr, start
+
+
+def block_vcycle(Hs, bounds, r: np.ndarray) -> np.ndarray:
+    """z = B r, B = blockdiag(B_0 .. B_{p-1}) over the row ranges ``bounds``."""
+    flats, arr, start = _blocks(Hs, bounds)
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    z = np.empty_like(r)
+    st = _lib().oracle_amg_block_vcycle(r.shape[0], len(Hs), _p(start),
+                                        ctypes.cast(arr, ctypes.c_void_p), _p(r), _p(z))
+    if st < 0:
+        raise ValueError("oracle_amg_block_vcycle: bad arguments")
+    return z
+
+
+def amg_block_solve(sys, b: np.ndarray, bounds, Hs, x0: Optional[np.ndarray] = None,
+                    tol: float = 1e-8, maxIter: int = 1000, norm: int = NORM_L2,
+                    history: bool = False, relTol: float = 0.0, minIter: int = 0,
+                    pipelined: bool = False):
+    """Block-Jacobi AMG-CG / AMG-PipeCG on the GLOBAL system ``sys`` with one local hierarchy per
+    row range (the distributed solve of reading Z33, emulated serially)."""
+    flats, arr, start = _blocks(Hs, bounds)
+    l, u, d, lo, up = _arrays(sys)
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(sys.nCells) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    it, res = ctypes.c_int(0), ctypes.c_double(0.0)
+    hist = np.full(maxIter + 1, np.nan) if history else None
+    st = _lib().oracle_amg_block_pcg(sys.nCells, l.shape[0], _p(l), _p(u), _p(d), _p(lo), _p(up),
+                                     _p(bb), _p(x), tol, maxIter, norm, ctypes.byref(it),
+                                     ctypes.byref(res), _p(hist), relTol, minIter, len(Hs),
+                                     _p(start), ctypes.cast(arr, ctypes.c_void_p),
+                                     1 if pipelined else 0)
+    if st < 0:
+        raise ValueError("oracle_amg_block_pcg: bad arguments")
+    if history:
+        return st, x, it.value, res.value, hist[: it.value + 1]
+    return st, x, it.value, res.value
+

@@ -501,3 +501,69 @@ int oracle_amg_pcg(int n, int nf, const int *l, const int *u, const double *diag
     free(buf);
     return st;
 }
+
+/* ---- block-Jacobi AMG across ranks (reading Z33) -------------------------------------------
+ * The distributed AMG preconditioner is block diagonal: rank g owns the contiguous rows
+ * [start[g], start[g+1]) and applies one V-cycle of the hierarchy built from its LOCAL matrix
+ * (interface couplings dropped).  The Krylov operator is the global matrix. */
+typedef struct { int nb; const int *start; const amg_t *H; } amg_blocks_t;
+
+static void amg_blocks_apply(const void *ctx, const double *r, double *z)
+{
+    const amg_blocks_t *B = (const amg_blocks_t *)ctx;
+    for (int g = 0; g < B->nb; ++g)
+        vcycle(&B->H[g], 0, r + B->start[g], z + B->start[g]);
+}
+
+static int amg_blocks_make(int n, int nb, const int *start, const amg_flat_t *const *F,
+                           amg_t **H, csr_t ***bufs)
+{
+    if (nb <= 0 || !start || !F || start[0] != 0 || start[nb] != n) return -1;
+    *H = malloc(sizeof(amg_t) * (size_t)nb);
+    *bufs = malloc(sizeof(csr_t *) * (size_t)nb);
+    for (int g = 0; g < nb; ++g) {
+        const int ng = start[g + 1] - start[g];
+        if (ng <= 0 || (F[g]->L > 0 && F[g]->n[0] != ng) || (F[g]->L == 0 && F[g]->nc != ng)) {
+            for (int k = 0; k < g; ++k) free((*bufs)[k]);
+            free(*H); free(*bufs);
+            return -1;
+        }
+        (*bufs)[g] = malloc(sizeof(csr_t) * (size_t)(3 * F[g]->L + 1));
+        (*H)[g] = amg_unflatten(F[g], (*bufs)[g]);
+    }
+    return 0;
+}
+
+/* z = B r with the block-diagonal preconditioner (exported for the pins). */
+int oracle_amg_block_vcycle(int n, int nb, const int *start, const amg_flat_t *const *F,
+                            const double *r, double *z)
+{
+    amg_t *H; csr_t **bufs;
+    if (amg_blocks_make(n, nb, start, F, &H, &bufs)) return OR_ERR_ARG;
+    amg_blocks_t B = {nb, start, H};
+    amg_blocks_apply(&B, r, z);
+    for (int g = 0; g < nb; ++g) free(bufs[g]);
+    free(bufs); free(H);
+    return OR_OK;
+}
+
+/* Block-Jacobi AMG-PCG / AMG-PipeCG on the global system (same criteria as oracle_amg_pcg). */
+int oracle_amg_block_pcg(int n, int nf, const int *l, const int *u, const double *diag,
+                         const double *lower, const double *upper, const double *b, double *x,
+                         double tol, int maxIter, int norm, int *nIter, double *finalRes,
+                         double *hist, double relTol, int minIter, int nb, const int *start,
+                         const amg_flat_t *const *F, int pipelined)
+{
+    amg_t *H; csr_t **bufs;
+    if (amg_blocks_make(n, nb, start, F, &H, &bufs)) return OR_ERR_ARG;
+    amg_blocks_t B = {nb, start, H};
+    prec_t M = {amg_blocks_apply, &B};
+    int st = pipelined ? pipecg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, 0,
+                                     nIter, finalRes, hist, relTol, minIter, &M)
+                       : pcg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, nIter,
+                                  finalRes, hist, relTol, minIter, &M);
+    for (int g = 0; g < nb; ++g) free(bufs[g]);
+    free(bufs); free(H);
+    return st;
+}
+

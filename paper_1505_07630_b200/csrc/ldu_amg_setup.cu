@@ -996,8 +996,7 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
   if (!o.maxLevels) o.maxLevels = LDU_AMG_MAX_LEVELS;
   if (!o.lanczosSteps) o.lanczosSteps = 20;
   if (!h->symmetric) fail_arg("AMG requires a symmetric matrix (lower == NULL or lower == upper)");
-  if (h->comm && h->comm->nRanks > 1)
-    throw Error(LDU_ERR_STATE, "AMG on multi-rank handles is not supported yet (reading Z33)");
+  // multi-rank: the hierarchy of the rank's local matrix (block-Jacobi, reading Z33)
   amg_release(h);
   cudaStream_t s = h->own_stream;
   cudaMemPool_t pool;

@@ -332,6 +332,53 @@ __global__ void __launch_bounds__(kBlock) k_amg_pipe_SU(
   finish_reduction<3>(v, rd, st);
 }
 
+// multi-rank classical: x += alpha_{k-1} p_{k-1}; p_k = z_k + beta_k p_{k-1} in place (the SpMV
+// with its halo exchange follows as a separate step)
+__global__ void __launch_bounds__(kBlock) k_amg_p(int n, const double* __restrict__ z,
+                                                  double* __restrict__ p, double* __restrict__ x,
+                                                  const State* st) {
+  if (st->done) return;
+  const double beta = st->beta, alpha = st->alpha;
+  GRID_STRIDE(c, n) {
+    const double po = p[c];
+    x[c] = fma(alpha, po, x[c]);
+    p[c] = fma(beta, po, z[c]);
+  }
+}
+
+// multi-rank pipelined: the GV recurrences with n = A m (incl. interfaces) already in nv
+__global__ void __launch_bounds__(kBlock) k_amg_pipe_U(
+    int n, const double* __restrict__ m, const double* __restrict__ nv, double* __restrict__ z,
+    double* __restrict__ q, double* __restrict__ s, double* __restrict__ p, double* __restrict__ x,
+    double* __restrict__ r, double* __restrict__ u, double* __restrict__ w, State* st, Red rd) {
+  if (st->done) return;
+  const double a = st->pa, b = st->pb;
+  const bool l2 = st->norm == LDU_NORM_L2;
+  double v[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(c, n) {
+    const double mc = m[c];
+    const double zc = fma(b, z[c], nv[c]);
+    const double qc = fma(b, q[c], mc);
+    const double sc = fma(b, s[c], w[c]);
+    const double pc = fma(b, p[c], u[c]);
+    z[c] = zc;
+    q[c] = qc;
+    s[c] = sc;
+    p[c] = pc;
+    x[c] = fma(a, pc, x[c]);
+    const double rc = fma(-a, sc, r[c]);
+    const double uc = fma(-a, qc, u[c]);
+    const double wc = fma(-a, zc, w[c]);
+    r[c] = rc;
+    u[c] = uc;
+    w[c] = wc;
+    v[0] = fma(rc, uc, v[0]);
+    v[1] = fma(wc, uc, v[1]);
+    v[2] += l2 ? rc * rc : fabs(rc);
+  }
+  finish_reduction<3>(v, rd, st);
+}
+
 // ---- V-cycle enqueue --------------------------------------------------------------------------
 // z0 = B f0 on stream s.  st != nullptr: every kernel exits at entry once the solve is done.
 // rho != nullptr: level-0 post-sweep (or the direct solve) also reduces (z0, f0) into rho's control.
@@ -414,7 +461,55 @@ void ensure_amg_work(ldu_handle h, bool pipelined) {
   }
 }
 
+// Multi-rank (block-Jacobi, reading Z33): the V-cycle is local; the SpMV exchanges the halo over
+// NCCL (amul_dev) and every reduction is an allgather of the local sums + the control kernel.
+// Pipelined: the allgather of iteration i's fused sums runs on the reduction stream while the
+// V-cycle m_i = B w_i and n_i = A m_i run (neither needs alpha_i, beta_i): P:97's overlap.
+long long enqueue_amg_iters_mr(ldu_handle h, bool pipelined, int batch, cudaStream_t s,
+                               bool profile) {
+  AmgHierarchy* H = h->amg;
+  ldu_comm cm = h->comm;
+  long long kernels = 0;
+  for (int it = 0; it < batch; ++it) {
+    prof_mark(h, profile, 4 * it + 0, s);
+    if (!pipelined) {
+      const Red rr = red_of(h, CTL_NONE, false, H->L ? h->gridA : h->grid);
+      kernels += enqueue_vcycle(h, h->r, H->zk, s, h->st, &rr);
+      prof_mark(h, profile, 4 * it + 1, s);
+      allgather_ctl(h, CTL_AMG_RHO, 1, s, kernels);
+      prof_mark(h, profile, 4 * it + 2, s);
+      k_amg_p<<<h->grid, kBlock, 0, s>>>(h->n, H->zk, h->p0, h->x, h->st);
+      ++kernels;
+      amul_dev(h, h->p0, h->q, s, kernels);
+      k_amg_dot<<<h->grid, kBlock, 0, s>>>(h->n, h->p0, h->q, h->st, red_of(h, CTL_NONE, false));
+      ++kernels;
+      allgather_ctl(h, CTL_CG_A, 1, s, kernels);
+      k_amg_passB<<<h->grid, kBlock, 0, s>>>(h->n, h->q, h->r, h->st, red_of(h, CTL_NONE, false));
+      ++kernels;
+      allgather_ctl(h, CTL_AMG_B, 1, s, kernels);
+    } else {
+      CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+      CUDA_CHECK(cudaStreamWaitEvent(h->red_stream, h->ev_fork, 0));
+      NCCL_CHECK(ncclAllGather(h->sums, h->gsums, kMaxVals, ncclDouble, cm->red, h->red_stream));
+      CUDA_CHECK(cudaEventRecord(h->ev_red, h->red_stream));
+      h->stats.allreduces++;
+      kernels += enqueue_vcycle(h, h->w, H->m, s, h->st, nullptr);
+      amul_dev(h, H->m, h->nv, s, kernels);
+      prof_mark(h, profile, 4 * it + 1, s);
+      CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_red, 0));
+      k_ctl<<<1, 32, 0, s>>>(CTL_PIPE_NEXT, h->st, h->gsums, cm->nRanks, 3);
+      prof_mark(h, profile, 4 * it + 2, s);
+      k_amg_pipe_U<<<h->grid, kBlock, 0, s>>>(h->n, H->m, h->nv, h->z, H->qk, h->s, h->p0, h->x,
+                                              h->r, H->u, h->w, h->st, red_of(h, CTL_NONE, false));
+      kernels += 2;
+    }
+    prof_mark(h, profile, 4 * it + 3, s);
+  }
+  return kernels;
+}
+
 long long enqueue_amg_iters(ldu_handle h, bool pipelined, int batch, cudaStream_t s, bool profile) {
+  if (multi(h)) return enqueue_amg_iters_mr(h, pipelined, batch, s, profile);
   AmgHierarchy* H = h->amg;
   long long kernels = 0;
   for (int it = 0; it < batch; ++it) {
@@ -497,7 +592,6 @@ ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, d
                      int maxIter, const ldu_solve_opts* opts, int* nIter, double* finalRes) {
   AmgHierarchy* H = h->amg;
   if (!H) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
-  if (multi(h)) throw Error(LDU_ERR_STATE, "AMG solves on multi-rank handles are not supported yet");
   if (!b || !x) fail_arg("b and x must not be NULL");
   if (!(tol >= 0.0)) fail_arg("tol must be >= 0");
   if (maxIter < 0) fail_arg("maxIter must be >= 0");
@@ -517,6 +611,8 @@ ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, d
 
   ensure_amg_work(h, pipelined);
   const int n = h->n;
+  const bool mr = multi(h);
+  if (mr && pipelined) ensure_vec(h->nv, n);
   cudaStream_t s = h->own_stream;
   h->stats = ldu_solve_stats{};
   long long kernels = 0;
@@ -566,22 +662,30 @@ ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, d
 
   // ---- r0 = b - A x0 and the criterion scale ---------------------------------------------
   double* sumA = pipelined ? h->nv : h->q;
+  double* Ax0 = h->ybuf;
   if (o.norm == LDU_NORM_OPENFOAM) {
     k_fill<<<small_grid(n), kBlock, 0, s>>>(n, 1.0, h->r);
     ++kernels;
     amul_dev(h, h->r, sumA, s, kernels);
-    k_sum_x<<<h->grid, kBlock, 0, s>>>(n, h->x, h->st, red_of(h, CTL_XBAR, true));
+    k_sum_x<<<h->grid, kBlock, 0, s>>>(n, h->x, h->st, red_of(h, CTL_XBAR, !mr));
     ++kernels;
+    if (mr) allgather_ctl(h, CTL_XBAR, 2, s, kernels);
   }
-  amul_dev(h, h->x, h->ybuf, s, kernels);
-  k_resid<<<h->grid, kBlock, 0, s>>>(n, bin, h->ybuf, sumA, h->rD, h->r, h->st,
-                                     red_of(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, true));
+  amul_dev(h, h->x, Ax0, s, kernels);
+  k_resid<<<h->grid, kBlock, 0, s>>>(n, bin, Ax0, sumA, h->rD, h->r, h->st,
+                                     red_of(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, !mr));
   ++kernels;
+  if (mr) allgather_ctl(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, 3, s, kernels);
   if (pipelined) {  // u0 = B r0; w0 = A u0; first fused reduction
     kernels += enqueue_vcycle(h, h->r, H->u, s, h->st, nullptr);
-    launch_amul(h, H->u, h->w, s);
-    k_amg_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->r, H->u, h->w, h->st, red_of(h, CTL_PIPE_TOP, true));
-    kernels += 2;
+    amul_dev(h, H->u, h->w, s, kernels);
+    k_amg_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->r, H->u, h->w, h->st,
+                                               red_of(h, CTL_PIPE_TOP, !mr));
+    ++kernels;
+    if (mr) {  // its allgather is issued by the first loop trip; k = -1 so that trip evaluates i = 0
+      static const int minus_one = -1;
+      CUDA_CHECK(cudaMemcpyAsync(&h->st->k, &minus_one, sizeof(int), cudaMemcpyHostToDevice, s));
+    }
   }
   CUDA_CHECK(cudaGetLastError());
   CUDA_CHECK(cudaEventRecord(h->ev[1], s));
@@ -610,12 +714,15 @@ ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, d
   }
   std::vector<float> passT;
   int batches = 0;
+  // multi-rank pipelined needs one more trip: the decision on r_i is taken after trip i's allgather
+  const long long trips = (long long)maxIter + ((pipelined && mr) ? 1 : 0);
+  const long long redPerIter = mr ? (pipelined ? 0 : 3) : 0;  // pipelined counted at enqueue
   if (maxIter > 0) {
     for (;;) {
       CUDA_CHECK(cudaGraphLaunch(H->graph[gi], s));
       ++batches;
       if (tol == 0.0 && !profile && o.relTol == 0.0) {  // fixed iterations: sync at the end only
-        if ((long long)batches * batch >= maxIter) break;
+        if ((long long)batches * batch >= trips) break;
         continue;
       }
       CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
@@ -628,11 +735,12 @@ ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, d
             passT.push_back(ms);
           }
       if (sh->done) break;
-      if ((long long)batches * batch >= (long long)maxIter + batch) break;  // safety net
+      if ((long long)batches * batch >= trips + batch) break;  // safety net
     }
   }
   CUDA_CHECK(cudaEventRecord(h->ev[2], s));
-  k_cg_final<<<small_grid(n), kBlock, 0, s>>>(n, h->p0, h->p1, h->x, h->st);
+  // pending x update (classical; multi-rank keeps p in place in p0) / x = 0 when b = 0
+  k_cg_final<<<small_grid(n), kBlock, 0, s>>>(n, h->p0, mr ? h->p0 : h->p1, h->x, h->st);
   ++kernels;
   CUDA_CHECK(cudaMemcpyAsync(sh, h->st, sizeof(State), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaMemcpyAsync(x, h->x, sizeof(double) * n, xd ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
@@ -650,10 +758,11 @@ ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, d
   CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]));
   h->stats.iterMs = ms;
   h->stats.kernels = kernels + (long long)batches * H->graphKernels[gi];
-  h->stats.allreduces = 0;
+  h->stats.allreduces = mr ? (long long)batches * batch * (pipelined ? 1 : redPerIter) : 0;
   h->stats.iterations = sh->iter;
   if (profile)  // pass 0 = V-cycle, pass 1 = Krylov passes, over the iterations that did work
-    for (long long g = 0; g < sh->iter && g < (long long)passT.size() / 2; ++g)
+    for (long long g = (pipelined && mr) ? 1 : 0;
+         g < sh->iter + ((pipelined && mr) ? 1 : 0) && g < (long long)passT.size() / 2; ++g)
       for (int p = 0; p < 2; ++p) {
         h->stats.passMs[p] += passT[2 * g + p];
         h->stats.passLaunches[p] += 1;

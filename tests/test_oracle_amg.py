@@ -306,3 +306,48 @@ def test_table2_amg_rows_band():
     assert 21 <= its[64][0] <= 35
     assert its[128][0] / its[64][0] <= 1.5
     assert all(itj >= 4 * it for it, itj in its.values())
+
+
+# ---- block-Jacobi AMG across ranks (reading Z33) ------------------------------------------------
+def _slab_case(p):
+    g = meshgen.hex_laplacian(12, 10, 9, conductance_sigma=0.4, seed=11, dirichlet=dict(x0=1.0))
+    parts = meshgen.slab_partition(g, p)
+    bounds = meshgen.slab_bounds(g.nCells, p)
+    return g, parts, bounds
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_block_preconditioner_is_block_diagonal_symmetric_spd(p):
+    g, parts, bounds = _slab_case(p)
+    Hs = amg.block_hierarchies(parts)
+    rng = np.random.default_rng(3)
+    n = g.nCells
+    for blk in range(p):                       # support stays inside the block
+        r = np.zeros(n)
+        lo, hi = bounds[blk], bounds[blk + 1]
+        r[lo:hi] = rng.uniform(-1, 1, hi - lo)
+        z = amg.block_vcycle(Hs, bounds, r)
+        assert np.all(z[:lo] == 0) and np.all(z[hi:] == 0) and np.linalg.norm(z[lo:hi]) > 0
+    x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    Bx, By = amg.block_vcycle(Hs, bounds, x), amg.block_vcycle(Hs, bounds, y)
+    assert abs(y @ Bx - x @ By) <= 1e-12 * abs(y @ Bx)     # symmetric
+    for _ in range(5):                                      # positive definite
+        r = rng.uniform(-1, 1, n)
+        assert r @ amg.block_vcycle(Hs, bounds, r) > 0
+
+
+@pytest.mark.parametrize("p", [2, 3])
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_block_amg_cg_against_direct_solve(p, pipelined):
+    g, parts, bounds = _slab_case(p)
+    Hs = amg.block_hierarchies(parts)
+    st, x, it, res = amg.amg_block_solve(g, g.b, bounds, Hs, tol=1e-12, maxIter=300,
+                                         pipelined=pipelined)
+    assert st == oracle.OK
+    xd = np.linalg.solve(amg.csr_of_ldu(g).toarray(), g.b)
+    assert np.linalg.norm(x - xd) <= 1e-9 * np.linalg.norm(xd)
+    # the block preconditioner is weaker than the global hierarchy, but still far better than
+    # Jacobi on this mesh
+    _, _, it_glob, _ = amg.amg_solve(g, g.b, tol=1e-12, maxIter=300)
+    _, _, it_jac, _ = oracle.pcg(g, g.b, tol=1e-12, maxIter=3000)
+    assert it_glob <= it <= it_jac // 2, (it_glob, it, it_jac)
