@@ -172,6 +172,95 @@ CsrMat assemble(int nrows, int ncols, long long m, unsigned long long* keys, dou
   return out;
 }
 
+// expansion entries per chunk of the row-wise assembly (LDU_AMG_CHUNK overrides; tests use tiny
+// chunks to check that chunking does not change a single bit)
+long long chunk_budget() {
+  static long long v = [] {
+    const char* e = std::getenv("LDU_AMG_CHUNK");
+    const long long b = e ? std::atoll(e) : 0;
+    return b > 0 ? b : (1LL << 28);
+  }();
+  return v;
+}
+
+__global__ void k_ptr_shift(int rows, const int* __restrict__ src, int add, int* __restrict__ dst) {
+  GSTRIDE(i, rows) dst[i] = src[i] + add;
+}
+
+// Row-wise sparse assembly in chunks of whole rows: count(cnt) writes every row's expansion size;
+// fill(r0, r1, off, key, val) writes the triples of rows [r0, r1) with keys (r - r0) * ncols + col
+// starting at off[r] - off[r0], in a fixed order.  Rows never straddle chunks and each chunk is
+// sorted (stable) and summed on its own, so the result is bitwise the one-shot assembly's while
+// the scratch stays bounded by the chunk budget.
+template <class Count, class Fill>
+CsrMat assemble_rows(int nrows, int ncols, bool drop, cudaStream_t s, Count count, Fill fill) {
+  Scratch sc(s);
+  long long* cnt = sc.get<long long>(nrows + 1);
+  long long* off = sc.get<long long>(nrows + 1);
+  count(cnt);
+  exclusive_scan<long long>(cnt, off, nrows, s);
+  const long long total = d2h(off + nrows, s);
+  const long long budget = chunk_budget();
+  if (total <= budget) {
+    Scratch c(s);
+    unsigned long long* key = c.get<unsigned long long>(total);
+    double* val = c.get<double>(total);
+    fill(0, nrows, off, key, val);
+    CUDA_CHECK(cudaGetLastError());
+    return assemble(nrows, ncols, total, key, val, drop, s);
+  }
+  std::vector<CsrMat> pieces;
+  std::vector<int> starts;
+  try {
+    for (int r0 = 0; r0 < nrows;) {
+      const long long base = d2h(off + r0, s);
+      int lo = r0 + 1, hi = nrows;  // largest r1 with off[r1] - base <= budget (at least r0 + 1)
+      while (lo < hi) {
+        const int mid = lo + (hi - lo + 1) / 2;
+        if (d2h(off + mid, s) - base <= budget) lo = mid;
+        else hi = mid - 1;
+      }
+      const int r1 = lo;
+      const long long m = d2h(off + r1, s) - base;
+      Scratch c(s);
+      unsigned long long* key = c.get<unsigned long long>(m);
+      double* val = c.get<double>(m);
+      fill(r0, r1, off, key, val);
+      CUDA_CHECK(cudaGetLastError());
+      pieces.push_back(assemble(r1 - r0, ncols, m, key, val, drop, s));
+      starts.push_back(r0);
+      r0 = r1;
+    }
+    CsrMat out;
+    out.nrows = nrows;
+    out.ncols = ncols;
+    for (const CsrMat& pc : pieces) out.nnz += pc.nnz;
+    if (out.nnz >= (1LL << 31) - 1) throw Error(LDU_ERR_OOM, "AMG level exceeds 2^31 stored entries");
+    out.ptr = dmalloc<int>(nrows + 1);
+    out.col = dmalloc<int>(out.nnz);
+    out.val = dmalloc<double>(out.nnz);
+    long long at = 0;
+    for (size_t k = 0; k < pieces.size(); ++k) {
+      const CsrMat& pc = pieces[k];
+      if (pc.nnz) {
+        CUDA_CHECK(cudaMemcpyAsync(out.col + at, pc.col, sizeof(int) * pc.nnz, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(out.val + at, pc.val, sizeof(double) * pc.nnz, cudaMemcpyDeviceToDevice, s));
+      }
+      k_ptr_shift<<<nblk(pc.nrows), kSB, 0, s>>>(pc.nrows, pc.ptr, (int)at, out.ptr + starts[k]);
+      at += pc.nnz;
+    }
+    const int last = (int)out.nnz;
+    CUDA_CHECK(cudaMemcpyAsync(out.ptr + nrows, &last, sizeof(int), cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    for (CsrMat& pc : pieces) pc.release();
+    out.group = group_of(out.nnz, nrows);
+    return out;
+  } catch (...) {
+    for (CsrMat& pc : pieces) pc.release();
+    throw;
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // level 0: CSR (diag included) from the handle's layout
 // ---------------------------------------------------------------------------------------------
@@ -223,11 +312,13 @@ __global__ void k_l0_count(Fmt A, long long* __restrict__ cnt) {
 }
 
 template <class Fmt>
-__global__ void k_l0_fill(Fmt A, const double* __restrict__ diag, const long long* __restrict__ off,
-                          unsigned long long* __restrict__ key, double* __restrict__ val) {
-  GSTRIDE(c, A.n) {
-    long long o = off[c];
-    const unsigned long long rowk = (unsigned long long)c * (unsigned long long)A.n;
+__global__ void k_l0_fill(Fmt A, const double* __restrict__ diag, int r0, int r1,
+                          const long long* __restrict__ off, unsigned long long* __restrict__ key,
+                          double* __restrict__ val) {
+  GSTRIDE(cc, r1 - r0) {
+    const long long c = r0 + cc;
+    long long o = off[c] - off[r0];
+    const unsigned long long rowk = (unsigned long long)cc * (unsigned long long)A.n;
     bool diagDone = false;
     for_row(A, (int)c, [&](int j, double a) {
       if (!diagDone && j > c) {
@@ -275,18 +366,15 @@ void with_layout(ldu_handle h, F&& f) {
 }
 
 CsrMat level0_csr(ldu_handle h, cudaStream_t s) {
-  Scratch sc(s);
   const int n = h->n;
-  long long* cnt = sc.get<long long>(n + 1);
-  long long* off = sc.get<long long>(n + 1);
-  with_layout(h, [&](auto A) { k_l0_count<<<nblk(n), kSB, 0, s>>>(A, cnt); });
-  exclusive_scan<long long>(cnt, off, n, s);
-  const long long m = d2h(off + n, s);
-  unsigned long long* key = sc.get<unsigned long long>(m);
-  double* val = sc.get<double>(m);
-  with_layout(h, [&](auto A) { k_l0_fill<<<nblk(n), kSB, 0, s>>>(A, h->diag, off, key, val); });
-  CUDA_CHECK(cudaGetLastError());
-  return assemble(n, n, m, key, val, false, s);
+  return assemble_rows(
+      n, n, false, s,
+      [&](long long* cnt) { with_layout(h, [&](auto A) { k_l0_count<<<nblk(n), kSB, 0, s>>>(A, cnt); }); },
+      [&](int r0, int r1, const long long* off, unsigned long long* key, double* val) {
+        with_layout(h, [&](auto A) {
+          k_l0_fill<<<nblk(r1 - r0), kSB, 0, s>>>(A, h->diag, r0, r1, off, key, val);
+        });
+      });
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -663,14 +751,20 @@ __global__ void k_diag_of(CsrView A, double* __restrict__ diag, double* __restri
   }
 }
 
-// S = A T expansion (smoothed) or T (unsmoothed): row i, key (i, agg[j]) in A's column order
-__global__ void k_expand_AT(CsrView A, int nAgg, const int* __restrict__ agg,
-                            unsigned long long* __restrict__ key, double* __restrict__ val) {
-  GSTRIDE(i, A.n) {
-    const unsigned long long rk = (unsigned long long)i * nAgg;
+// S = A T expansion (smoothed): row i, key (i, agg[j]) in A's column order
+__global__ void k_count_row(CsrView A, long long* __restrict__ cnt) {
+  GSTRIDE(i, A.n) cnt[i] = A.ptr[i + 1] - A.ptr[i];
+}
+__global__ void k_expand_AT(CsrView A, int nAgg, const int* __restrict__ agg, int r0, int r1,
+                            const long long* __restrict__ off, unsigned long long* __restrict__ key,
+                            double* __restrict__ val) {
+  GSTRIDE(ii, r1 - r0) {
+    const long long i = r0 + ii;
+    const unsigned long long rk = (unsigned long long)ii * nAgg;
+    long long o = off[i] - off[r0];
     for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-      key[k] = rk + agg[A.col[k]];
-      val[k] = A.val[k];
+      key[o] = rk + agg[A.col[k]];
+      val[o++] = A.val[k];
     }
   }
 }
@@ -766,11 +860,13 @@ __global__ void k_count_AP(CsrView A, const int* __restrict__ Pptr, long long* _
     cnt[i] = c;
   }
 }
-__global__ void k_expand_AP(CsrView A, CsrView P, int ncols, const long long* __restrict__ off,
-                            unsigned long long* __restrict__ key, double* __restrict__ val) {
-  GSTRIDE(i, A.n) {
-    long long o = off[i];
-    const unsigned long long rk = (unsigned long long)i * ncols;
+__global__ void k_expand_AP(CsrView A, CsrView P, int ncols, int r0, int r1,
+                            const long long* __restrict__ off, unsigned long long* __restrict__ key,
+                            double* __restrict__ val) {
+  GSTRIDE(ii, r1 - r0) {
+    const long long i = r0 + ii;
+    long long o = off[i] - off[r0];
+    const unsigned long long rk = (unsigned long long)ii * ncols;
     for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
       const int j = A.col[k];
       const double a = A.val[k];
@@ -782,21 +878,32 @@ __global__ void k_expand_AP(CsrView A, CsrView P, int ncols, const long long* __
   }
 }
 
-// expansion of P^T (A P): row i of P and of AP -> (I, J) += p_iI * ap_iJ
-__global__ void k_count_PtAP(int n, const int* __restrict__ Pptr, const int* __restrict__ Qptr,
-                             long long* __restrict__ cnt) {
-  GSTRIDE(i, n) cnt[i] = (long long)(Pptr[i + 1] - Pptr[i]) * (Qptr[i + 1] - Qptr[i]);
+// A_c = R (A P), row-wise over coarse rows I: (I, J) += R_Ii (AP)_iJ, i ascending then J.  For a
+// given (I, J) the contributions come in ascending i -- the same order as expanding P^T (A P) by
+// fine rows, so the sums are the same bitwise.
+__global__ void k_count_RAP(CsrView R, const int* __restrict__ Qptr, long long* __restrict__ cnt) {
+  GSTRIDE(I, R.n) {
+    long long c = 0;
+    for (int t = R.ptr[I]; t < R.ptr[I + 1]; ++t) {
+      const int i = R.col[t];
+      c += Qptr[i + 1] - Qptr[i];
+    }
+    cnt[I] = c;
+  }
 }
-__global__ void k_expand_PtAP(CsrView P, CsrView Q, int nc, const long long* __restrict__ off,
-                              unsigned long long* __restrict__ key, double* __restrict__ val) {
-  GSTRIDE(i, P.n) {
-    long long o = off[i];
-    for (int m = P.ptr[i]; m < P.ptr[i + 1]; ++m) {
-      const unsigned long long rk = (unsigned long long)P.col[m] * nc;
-      const double p = P.val[m];
-      for (int t = Q.ptr[i]; t < Q.ptr[i + 1]; ++t) {
-        key[o] = rk + Q.col[t];
-        val[o++] = p * Q.val[t];
+__global__ void k_expand_RAP(CsrView R, CsrView Q, int nc, int r0, int r1,
+                             const long long* __restrict__ off, unsigned long long* __restrict__ key,
+                             double* __restrict__ val) {
+  GSTRIDE(II, r1 - r0) {
+    const long long I = r0 + II;
+    long long o = off[I] - off[r0];
+    const unsigned long long rk = (unsigned long long)II * nc;
+    for (int t = R.ptr[I]; t < R.ptr[I + 1]; ++t) {
+      const int i = R.col[t];
+      const double rv = R.val[t];
+      for (int u = Q.ptr[i]; u < Q.ptr[i + 1]; ++u) {
+        key[o] = rk + Q.col[u];
+        val[o++] = rv * Q.val[u];
       }
     }
   }
@@ -812,10 +919,11 @@ CsrMat build_P(const CsrMat& A, const int* agg, int nAgg, const double* diag, do
     k_expand_T<<<nblk(n), kSB, 0, s>>>(n, nAgg, agg, key, val);
     return assemble(n, nAgg, n, key, val, false, s);
   }
-  unsigned long long* key = sc.get<unsigned long long>(A.nnz);
-  double* val = sc.get<double>(A.nnz);
-  k_expand_AT<<<nblk(n), kSB, 0, s>>>(view(A), nAgg, agg, key, val);
-  CsrMat P = assemble(n, nAgg, A.nnz, key, val, false, s);  // S = A T
+  CsrMat P = assemble_rows(  // S = A T
+      n, nAgg, false, s, [&](long long* cnt) { k_count_row<<<nblk(n), kSB, 0, s>>>(view(A), cnt); },
+      [&](int r0, int r1, const long long* off, unsigned long long* key, double* val) {
+        k_expand_AT<<<nblk(r1 - r0), kSB, 0, s>>>(view(A), nAgg, agg, r0, r1, off, key, val);
+      });
   int* zeros = sc.get<int>(1);
   CUDA_CHECK(cudaMemsetAsync(zeros, 0, sizeof(int), s));
   k_finish_P<<<nblk(n), kSB, 0, s>>>(view(P), agg, diag, omega, P.val, zeros);
@@ -832,36 +940,26 @@ CsrMat transpose(const CsrMat& P, cudaStream_t s) {
   return assemble(P.ncols, P.nrows, P.nnz, key, val, false, s);
 }
 
-CsrMat galerkin(const CsrMat& A, const CsrMat& P, cudaStream_t s) {
+CsrMat galerkin(const CsrMat& A, const CsrMat& P, const CsrMat& R, cudaStream_t s) {
   const int n = A.nrows, nc = P.ncols;
-  CsrMat AP;
-  {
-    Scratch sc(s);
-    long long* cnt = sc.get<long long>(n + 1);
-    long long* off = sc.get<long long>(n + 1);
-    k_count_AP<<<nblk(n), kSB, 0, s>>>(view(A), P.ptr, cnt);
-    exclusive_scan<long long>(cnt, off, n, s);
-    const long long m = d2h(off + n, s);
-    unsigned long long* key = sc.get<unsigned long long>(m);
-    double* val = sc.get<double>(m);
-    k_expand_AP<<<nblk(n), kSB, 0, s>>>(view(A), view(P), nc, off, key, val);
-    AP = assemble(n, nc, m, key, val, true, s);
-  }
-  CsrMat Ac;
-  {
-    Scratch sc(s);
-    long long* cnt = sc.get<long long>(n + 1);
-    long long* off = sc.get<long long>(n + 1);
-    k_count_PtAP<<<nblk(n), kSB, 0, s>>>(n, P.ptr, AP.ptr, cnt);
-    exclusive_scan<long long>(cnt, off, n, s);
-    const long long m = d2h(off + n, s);
-    unsigned long long* key = sc.get<unsigned long long>(m);
-    double* val = sc.get<double>(m);
-    k_expand_PtAP<<<nblk(n), kSB, 0, s>>>(view(P), view(AP), nc, off, key, val);
+  CsrMat AP = assemble_rows(
+      n, nc, true, s, [&](long long* cnt) { k_count_AP<<<nblk(n), kSB, 0, s>>>(view(A), P.ptr, cnt); },
+      [&](int r0, int r1, const long long* off, unsigned long long* key, double* val) {
+        k_expand_AP<<<nblk(r1 - r0), kSB, 0, s>>>(view(A), view(P), nc, r0, r1, off, key, val);
+      });
+  try {
+    CsrMat Ac = assemble_rows(
+        nc, nc, true, s,
+        [&](long long* cnt) { k_count_RAP<<<nblk(nc), kSB, 0, s>>>(view(R), AP.ptr, cnt); },
+        [&](int r0, int r1, const long long* off, unsigned long long* key, double* val) {
+          k_expand_RAP<<<nblk(r1 - r0), kSB, 0, s>>>(view(R), view(AP), nc, r0, r1, off, key, val);
+        });
     AP.release();
-    Ac = assemble(nc, nc, m, key, val, true, s);
+    return Ac;
+  } catch (...) {
+    AP.release();
+    throw;
   }
-  return Ac;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1041,7 +1139,7 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
       L.P = build_P(A, agg, nAgg, diag, L.omega, !o.unsmoothed, s);
       L.R = transpose(L.P, s);
       tr.mark("P,R", (int)H->lv.size());
-      CsrMat Ac = galerkin(A, L.P, s);
+      CsrMat Ac = galerkin(A, L.P, L.R, s);
       tr.mark("galerkin", (int)H->lv.size());
       L.r = dmalloc<double>(n);
       L.x = dmalloc<double>(n);

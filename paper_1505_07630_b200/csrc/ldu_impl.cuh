@@ -162,7 +162,7 @@ struct ldu_handle_s {
   int chunkK = 2048;                  // variant 5: rows per chunk
   bool fusePipe = true;               // single rank: pipelined S+U fused (LDU_PIPE_FUSE)
   bool persist = false;               // single rank: persistent cooperative kernels
-  bool pdl = true;                    // programmatic dependent launch in the multi-rank loop
+  bool pdl = false;                   // programmatic dependent launch in the multi-rank loop (LDU_PDL=1)
   int gridP = 0;                      // co-resident grid of the persistent kernels
   double* ppartials = nullptr;        // [2][kMaxVals][gridP]
   // history

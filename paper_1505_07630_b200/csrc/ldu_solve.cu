@@ -1802,7 +1802,10 @@ void configure(ldu_handle h) {
   h->chunkK = 2048;
   h->fusePipe = true;
   if (const char* v = std::getenv("LDU_PIPE_FUSE")) h->fusePipe = std::atoi(v) != 0;
-  h->pdl = true;
+  // PDL on the multi-rank fused pipelined chain is opt-in: measured +0.7 % at 256^3 / 4 ranks,
+  // but at 512^3 / 4 ranks it produced a wrong iterate (BREAKDOWN after 18 iterations, then a
+  // peer wait timeout) that LDU_PDL=0 does not (profiles/r01_amg/SUMMARY.md)
+  h->pdl = false;
   if (const char* v = std::getenv("LDU_PDL")) h->pdl = std::atoi(v) != 0;
   // persistent cooperative kernels for single-rank, latency-bound sizes (LDU_PERSIST=0/1 forces)
   h->persist = !(h->comm && h->comm->nRanks > 1) && (long long)h->n * 80 < (long long)prop.l2CacheSize;

@@ -308,3 +308,39 @@ def test_amg_full_size_256(ldu):
             assert true < 2e-10, true
             its.append(it)
         assert abs(its[0] - its[1]) <= 1 and 25 <= its[0] <= 45, its
+
+
+_CHUNK_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import meshgen, paper_1505_07630_b200 as ldu
+torch.cuda.set_device(0)
+s = meshgen.hex_laplacian(23, 17, 11, conductance_sigma=0.5, seed=3)
+with ldu.LduMatrix.from_system(s) as A:
+    info = A.amg_setup()
+    out = {{}}
+    for l in range(info["nLevels"] + 1):
+        for w in ("A",) + (("P", "R") if l < info["nLevels"] else ()):
+            p, c, v = A.amg_matrix(l, w)
+            out[f"{{w}}{{l}}_p"], out[f"{{w}}{{l}}_c"], out[f"{{w}}{{l}}_v"] = p, c, v
+    np.savez({path!r}, **out)
+"""
+
+
+def test_chunked_assembly_is_bitwise_identical(ldu, tmp_path):
+    """The row-chunked sparse products (bounded scratch for 512^3) give the same hierarchy, bit
+    for bit, as the one-shot assembly: rows never straddle chunks and sums keep their order."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    res = {}
+    for chunk in ("0", "700"):
+        path = str(tmp_path / f"h{chunk}.npz")
+        env = dict(os.environ, LDU_AMG_CHUNK=chunk)
+        p = subprocess.run([sys.executable, "-c", _CHUNK_SCRIPT.format(root=ROOT, path=path)],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[chunk] = np.load(path)
+    assert sorted(res["0"].files) == sorted(res["700"].files)
+    for k in res["0"].files:
+        np.testing.assert_array_equal(res["0"][k], res["700"][k], err_msg=k)
