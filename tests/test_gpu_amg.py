@@ -327,20 +327,29 @@ with ldu.LduMatrix.from_system(s) as A:
 """
 
 
-def test_chunked_assembly_is_bitwise_identical(ldu, tmp_path):
-    """The row-chunked sparse products (bounded scratch for 512^3) give the same hierarchy, bit
-    for bit, as the one-shot assembly: rows never straddle chunks and sums keep their order."""
+def test_setup_paths_are_bitwise_identical(ldu, tmp_path):
+    """The direct level-0 CSR, the sort-based assembly and its row-chunked form (bounded scratch
+    for 512^3) build the same hierarchy bit for bit: every path sums a coefficient's products in
+    expansion order and rows never straddle chunks."""
     import subprocess
     import sys
     from conftest import ROOT
     res = {}
-    for chunk in ("0", "700"):
-        path = str(tmp_path / f"h{chunk}.npz")
-        env = dict(os.environ, LDU_AMG_CHUNK=chunk)
+    # default (direct level-0 CSR, one-shot sort-based products), level 0 through the sort-based
+    # assembly too, and everything in 700-entry chunks: the same bits
+    for chunk, sort_only in (("0", ""), ("0", "1"), ("700", "1")):
+        key = chunk + sort_only
+        path = str(tmp_path / f"h{key}.npz")
+        env = {k: v for k, v in os.environ.items()
+               if k not in ("LDU_AMG_SORT_L0", "LDU_AMG_CHUNK")}
+        env["LDU_AMG_CHUNK"] = chunk
+        if sort_only == "1":
+            env["LDU_AMG_SORT_L0"] = "1"
         p = subprocess.run([sys.executable, "-c", _CHUNK_SCRIPT.format(root=ROOT, path=path)],
                            env=env, capture_output=True, text=True, timeout=300)
         assert p.returncode == 0, p.stderr[-2000:]
-        res[chunk] = np.load(path)
-    assert sorted(res["0"].files) == sorted(res["700"].files)
-    for k in res["0"].files:
-        np.testing.assert_array_equal(res["0"][k], res["700"][k], err_msg=k)
+        res[key] = np.load(path)
+    for other in ("01", "7001"):
+        assert sorted(res["0"].files) == sorted(res[other].files)
+        for k in res["0"].files:
+            np.testing.assert_array_equal(res["0"][k], res[other][k], err_msg=f"{other} {k}")
