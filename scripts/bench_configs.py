@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Measurements of the BASELINE.json configs other than the bench.py headline (config 3).
 
-    python scripts/bench_configs.py c1|c2|c5            (1 GPU)
+    python scripts/bench_configs.py c1|c2|c5|c2amg|c5amg (1 GPU)
     torchrun --nproc-per-node N scripts/bench_configs.py c4   (512^3 z-slabs over N GPUs)
 
 Prints one JSON line per measurement (rank 0).  Times are device times (CUDA events on the
@@ -142,6 +142,79 @@ def c5(ldu, n=200, iters=300):
                           "generation_s": gen}), flush=True)
 
 
+def amg_vs_jacobi(ldu, A, s, b, label, tol=1e-8, extra=None):
+    """Time to solution (device) of Jacobi-PCG vs AMG-PCG / AMG-PipeCG, x0 = 0, and the AMG setup."""
+    st = torch.cuda.current_stream()
+    t0 = time.time()
+    info = A.amg_setup()
+    wall = time.time() - t0
+    for name, fn in (("jacobi_pcg", A.pcg_solve), ("amg_pcg", A.amg_pcg_solve),
+                     ("amg_pipecg", A.amg_pipecg_solve)):
+        x = torch.zeros_like(b)
+        fn(b, x, tol=tol, maxIter=100000)
+        its = []
+
+        def run():
+            x.zero_()
+            _, it, _ = fn(b, x, tol=tol, maxIter=100000)
+            its.append(it)
+        t, _ = ev_time(st, run, 3)
+        y = torch.empty_like(x)
+        A.amul(x, y)
+        true = float(torch.linalg.norm(b - y) / torch.linalg.norm(b))
+        d = {"config": label, "solver": name, "tol": tol, "iters": its[-1], "ms": 1e3 * t / 3,
+             "true_res": true}
+        if name.startswith("amg"):
+            d.update({"setup_ms": info["setupMs"], "setup_wall_s": wall, "levels": info["n"],
+                      "operator_complexity": info["operatorComplexity"]})
+        if extra:
+            d.update(extra)
+        print(json.dumps(d), flush=True)
+
+
+def c5amg(ldu, n=200):
+    """NEXT-2 on the irregular mesh (SELL-32 layout): AMG-PCG vs Jacobi-PCG to tol 1e-8."""
+    t0 = time.time()
+    s = meshgen.irregular_mesh(n, seed=1505)
+    gen = time.time() - t0
+    A = ldu.LduMatrix.from_system(s)
+    A.set_stream(torch.cuda.current_stream().cuda_stream)
+    b = torch.from_numpy(s.b).cuda()
+    amg_vs_jacobi(ldu, A, s, b, f"c5-like irregular {n}^3 base ({s.nCells:,} cells), RCM, "
+                  f"{A.info()['layout_name']}", extra={"generation_s": gen})
+
+
+def c2amg(ldu):
+    """icoFoam p / pFinal sequence (c2, 1024^2) with AMG-PCG: one setup for the constant pressure
+    matrix, 40 warm-started solves (OpenFOAM norm, tol 1e-6, relTol 0.05 then 0)."""
+    nx = ny = 1024
+    s = meshgen.cavity_pressure_2d(nx, ny)
+    A = ldu.LduMatrix.from_system(s)
+    st = torch.cuda.current_stream()
+    A.set_stream(st.cuda_stream)
+    info = A.amg_setup()
+    rhs = [torch.from_numpy(meshgen.cavity_rhs(nx, ny, t)).cuda() for t in range(20)]
+    for name, fn in (("jacobi_pcg", A.pcg_solve), ("amg_pcg", A.amg_pcg_solve)):
+        x = torch.zeros(s.nCells, dtype=torch.float64, device="cuda")
+        its = []
+
+        def piso():
+            x.zero_()
+            for t in range(20):
+                for rt in (0.05, 0.0):
+                    _, it, _ = fn(rhs[t], x, tol=1e-6, maxIter=100000, norm=ldu.NORM_OPENFOAM,
+                                  relTol=rt)
+                    its.append(it)
+        piso()
+        its.clear()
+        t, _ = ev_time(st, piso)
+        print(json.dumps({"config": "c2 cavity 1024^2, icoFoam p (relTol 0.05) / pFinal (relTol 0)",
+                          "solver": name, "norm": "OpenFOAM", "tol": 1e-6,
+                          "total_iters": int(sum(its)), "seconds_40_solves": t,
+                          "amg_setup_ms": info["setupMs"] if name == "amg_pcg" else None,
+                          "amg_levels": info["n"] if name == "amg_pcg" else None}), flush=True)
+
+
 def c4(ldu, iters=300):
     """512^3 z-slabs over N GPUs (torchrun), fixed iterations, both solvers."""
     import torch.distributed as dist
@@ -268,4 +341,5 @@ if __name__ == "__main__":
     if which == "c5het":
         c5dist(ldu, slow_rank_sms=int(sys.argv[2]) if len(sys.argv) > 2 else 40)
     else:
-        {"c1": c1, "c2": c2, "c4": c4, "c5": c5, "c5dist": c5dist}[which](ldu)
+        {"c1": c1, "c2": c2, "c4": c4, "c5": c5, "c5dist": c5dist, "c5amg": c5amg,
+         "c2amg": c2amg}[which](ldu)
