@@ -28,7 +28,7 @@ struct CsrMat {
   double* val = nullptr;  // [nnz]
   int group = 1;          // lanes per row of the CSR-vector SpMV (power of two <= 32)
   // optional SELL-32 copy for the V-cycle (coarse A_l with near-uniform rows): 32-row slices,
-  // lane-interleaved (col, val) pairs, padding = (own row, 0.0) so rows need no break test
+  // lane-interleaved (col, val) pairs, padding = (a column of the row, 0.0): no break test
   bool useSell = false;
   long long* slicePtr = nullptr;  // [nslices + 1] in pair rows
   int* npairs = nullptr;          // [nslices]

@@ -92,10 +92,16 @@ void exclusive_scan(const T* in, T* out, long long n, cudaStream_t s) {
 
 // lanes per row of the CSR-vector kernels: one trip of kCsrU entries per lane covers an average
 // row (kCsrU = 4 for one lane per row, 8 otherwise; ldu_amg_solve.cuh)
+double env_double(const char* name, double dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atof(e) : dflt;
+}
+
 int group_of(long long nnz, int rows) {
+  static const double per = env_double("LDU_AMG_LANE_ENTRIES", 16.0);  // measured: 8 -> 16 -1.5 %
   const double avg = rows ? (double)nnz / rows : 1.0;
   int g = 1;
-  while (g < 32 && (g == 1 ? 4.0 : 8.0 * g) < avg) g <<= 1;
+  while (g < 32 && (g == 1 ? 4.0 : per * g) < avg) g <<= 1;
   return g;
 }
 
@@ -754,7 +760,9 @@ __global__ void k_sell_fill(CsrView A, const long long* __restrict__ sp, const i
       const long long slot = ((sp[sl] + jj) * 32 + lane) * 2;
       for (int h = 0; h < 2; ++h) {
         const int k = b + 2 * jj + h;
-        col[slot + h] = k < e ? A.col[k] : (int)r;  // padding: own row, coefficient 0
+        // padding: coefficient 0 on a column the row already references (a valid index of the
+        // operand even for rectangular P / R; no other row's value can leak in as 0 * NaN)
+        col[slot + h] = k < e ? A.col[k] : (e > b ? A.col[b] : 0);
         val[slot + h] = k < e ? A.val[k] : 0.0;
       }
     }
@@ -1195,9 +1203,10 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
         L.f = dmalloc<double>(n);
         L.z = dmalloc<double>(n);
       }
-      attach_sell(L.R, 1.25, s);  // V-cycle copies where rows are near-uniform
-      attach_sell(L.P, 1.25, s);
-      attach_sell(Ac, 1.25, s);
+      static const double pad = env_double("LDU_AMG_SELL_PAD", 1.25);
+      attach_sell(L.R, pad, s);  // V-cycle copies where rows are near-uniform
+      attach_sell(L.P, pad, s);
+      attach_sell(Ac, pad, s);
       tr.mark("sell", (int)H->lv.size());
       H->lv.push_back(L);
       // next level's diagonal

@@ -114,7 +114,7 @@ struct EpiPost {  // K4: z = x + w rD (f - A x)
 };
 
 // SELL-32 rows (coarse A_l, see attach_sell): one row per thread, lane-interleaved pairs, 4 pair
-// loads in flight per trip; padding is (own row, 0) so there is no data-dependent exit
+// loads in flight per trip; padding is (a column of the row, 0): no data-dependent exit
 template <class Epi>
 __global__ void __launch_bounds__(kBlock) k_sell_rows(SellView A, Epi e, const State* st) {
   if (st && st->done) return;
