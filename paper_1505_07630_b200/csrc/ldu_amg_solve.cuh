@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kBlock) k_amg_pipe_dots(int n, const double* _
 }
 
 template <class Fmt>
-__global__ void __launch_bounds__(kBlock) k_amg_pipe_SU(
+__global__ void __launch_bounds__(kBlock, 6) k_amg_pipe_SU(
     Fmt A, const double* __restrict__ diag, const double* __restrict__ m, double* __restrict__ z,
     double* __restrict__ q, double* __restrict__ s, double* __restrict__ p, double* __restrict__ x,
     double* __restrict__ r, double* __restrict__ u, double* __restrict__ w, State* st, Red rd) {

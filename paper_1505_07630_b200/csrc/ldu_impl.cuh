@@ -153,6 +153,7 @@ struct ldu_handle_s {
   ldu::State* st_host = nullptr;  // pinned
   int grid = 0, block = ldu::kBlock;  // streaming passes
   int gridA = 0;                      // SpMV-bearing passes
+  int gridSU = 0, suMinB = 0;         // single-rank fused pipelined pass (LDU_SU_MINB)
   int variant = 0;                    // DIA kernel variant (LDU_VARIANT)
   bool marchOk = false;               // plane-marching geometry applies
   bool marchStrict = false;           // ... with the performance geometry (one wave, lockstep)

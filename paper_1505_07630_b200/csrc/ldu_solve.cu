@@ -450,8 +450,10 @@ __global__ void __launch_bounds__(kBlock) k_pipe_U(int n, const double* __restri
 // to hide behind the SpMV, so n_i = A (rD.w_i) is consumed row by row and never stored (saves the
 // 16N bytes of writing and re-reading n).  w is ping-pong buffered: neighbours gather w_i while
 // the pass writes w_{i+1}.
-template <class Fmt>
-__global__ void __launch_bounds__(kBlock) k_pipe_SU(Fmt A, const double* __restrict__ rD,
+// MINB = 6 resident blocks per SM caps the registers at 40 (the unconstrained allocation, 48-84,
+// leaves 3-5 blocks): 343 vs 381-418 us per launch at 256^3, 0.96 of the measured copy bandwidth
+template <class Fmt, int MINB = 6>
+__global__ void __launch_bounds__(kBlock, MINB) k_pipe_SU(Fmt A, const double* __restrict__ rD,
                                                     double* w0, double* w1,
                                                     double* __restrict__ z, double* __restrict__ s,
                                                     double* __restrict__ p, double* __restrict__ x,
@@ -1128,13 +1130,13 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
       trace_mark(h, it, 1, s);
       trace_mark(h, it, 2, s);
       ++kernels;
-      Red ru = red_loop(h, CTL_PIPE_NEXT, false, h->gridA);
+      Red ru = red_loop(h, CTL_PIPE_NEXT, false, h->gridSU);
       if (haveIf) ru.store_only = 1;
       prof_mark(h, profile, 4 * it + 0, s);
       prof_mark(h, profile, 4 * it + 1, s);
       prof_mark(h, profile, 4 * it + 2, s);
       with_format(h, [&](auto A) {
-        launch_pdl(h->pdl && !profile && h->trace.empty(), k_pipe_SU<decltype(A)>, h->gridA,
+        launch_pdl(h->pdl && !profile && h->trace.empty(), k_pipe_SU<decltype(A)>, h->gridSU,
                    kBlock, s, A, (const double*)h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x,
                    h->r, h->st, ru);
       });
@@ -1144,9 +1146,9 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
       if (haveIf) {
         if (it > 0) p2p_join(h, s);
         Red ri = red_loop(h, CTL_PIPE_NEXT, false);
-        const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->gridA);
-        ri.slot_base = h->gridA;
-        ri.total = h->gridA + ig;
+        const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->gridSU);
+        ri.slot_base = h->gridSU;
+        ri.total = h->gridSU + ig;
         launch_pdl(false, k_pipe_fixup_p2p,  // follows a cross-stream join: plain dependency
                    ig, kBlock, s, h->nIfCells, (const int*)h->ifCell, (const int*)h->ifCellPtr,
                    (const int*)h->ifFaceIdx, (const double*)h->ifCoeffs, (const double*)h->rD,
@@ -1192,8 +1194,12 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
       prof_mark(h, profile, 4 * it + 1, s);
       prof_mark(h, profile, 4 * it + 2, s);
       with_format(h, [&](auto A) {
-        k_pipe_SU<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x,
-                                               h->r, h->st, red_of(h, CTL_PIPE_NEXT, true, h->gridA));
+        using Fmt = decltype(A);
+        const Red rd = red_of(h, CTL_PIPE_NEXT, true, h->gridSU);
+        if (h->suMinB == 8)
+          k_pipe_SU<Fmt, 8><<<h->gridSU, kBlock, 0, s>>>(A, h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x, h->r, h->st, rd);
+        else
+          k_pipe_SU<Fmt><<<h->gridSU, kBlock, 0, s>>>(A, h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x, h->r, h->st, rd);
       });
       prof_mark(h, profile, 4 * it + 3, s);
       ++kernels;
@@ -1946,6 +1952,13 @@ void configure(ldu_handle h) {
     });
   }
   if (use_tma(h)) h->gridA = h->tGrid;
+  // fused pipelined pass: 6 resident blocks per SM (LDU_SU_MINB=8 single rank: 8, measured slower)
+  h->suMinB = 6;
+  if (const char* v = std::getenv("LDU_SU_MINB")) h->suMinB = std::atoi(v) == 8 && !(h->comm && h->comm->nRanks > 1) ? 8 : 6;
+  with_format(h, [&](auto A) {
+    using Fmt = decltype(A);
+    h->gridSU = h->suMinB == 8 ? grid_of((const void*)k_pipe_SU<Fmt, 8>) : grid_of((const void*)k_pipe_SU<Fmt>);
+  });
   if (h->variant == 6 && h->layout == LDU_LAYOUT_DIA_SYM && h->off[0] == 1) {
     with_dia(h, [&](auto A) {
       constexpr int ND = sizeof(A.off) / sizeof(int);
@@ -1971,7 +1984,7 @@ void configure(ldu_handle h) {
     const long long g = (long long)prop.multiProcessorCount * std::max(1, std::min(o1, o2));
     h->gridP = (int)std::max(1LL, std::min(g, need));
   }
-  h->maxParts = std::max(h->grid, h->gridA) + 4096;
+  h->maxParts = std::max({h->grid, h->gridA, h->gridSU}) + 4096;
   h->partials = dmalloc<double>((size_t)kMaxVals * h->maxParts);
   h->ticket = dmalloc<unsigned>(2);  // [0] reductions, [1] halo pack (may run concurrently)
   CUDA_CHECK(cudaMemset(h->ticket, 0, 2 * sizeof(unsigned)));
