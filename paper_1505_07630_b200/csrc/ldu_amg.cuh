@@ -93,6 +93,8 @@ struct AmgHierarchy {
   double setupMs = 0.0;
   // AMG Krylov work vectors (lazily allocated by the solves)
   double *u = nullptr, *m = nullptr, *zk = nullptr, *qk = nullptr;
+  // occupancy-sized grids of the level-0 kernels (set by the first V-cycle / solve)
+  int gPre = 0, gPost = 0, gPassA = 0, gPipe = 0;
   // iteration-batch graphs: [pipelined + 2 * profile]
   cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
   int graphBatch[4] = {0, 0, 0, 0};

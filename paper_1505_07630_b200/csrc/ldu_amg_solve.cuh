@@ -379,6 +379,31 @@ __global__ void __launch_bounds__(kBlock) k_amg_pipe_U(
   finish_reduction<3>(v, rd, st);
 }
 
+// resident blocks per SM x SMs, capped by the rows (grid-stride kernels)
+int occ_grid(ldu_handle h, const void* fn) {
+  int dev = 0, sms = 1, o = 1;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kBlock, 0));
+  const long long need = ((long long)h->n + kBlock - 1) / kBlock;
+  return (int)std::max(1LL, std::min((long long)sms * std::max(1, o), need));
+}
+
+void amg_grids(ldu_handle h) {
+  AmgHierarchy* H = h->amg;
+  if (H->gPre) return;
+  with_format(h, [&](auto A) {
+    using Fmt = decltype(A);
+    H->gPre = occ_grid(h, (const void*)k_vc_pre<Fmt>);
+    H->gPost = std::min(occ_grid(h, (const void*)k_vc_post<Fmt, true>),
+                        occ_grid(h, (const void*)k_vc_post<Fmt, false>));
+    H->gPassA = occ_grid(h, (const void*)k_amg_passA<Fmt>);
+    H->gPipe = occ_grid(h, (const void*)k_amg_pipe_SU<Fmt>);
+  });
+  if (std::max({H->gPre, H->gPost, H->gPassA, H->gPipe}) > h->maxParts)
+    throw Error(LDU_ERR_STATE, "AMG grid exceeds the reduction slots");
+}
+
 // ---- V-cycle enqueue --------------------------------------------------------------------------
 // z0 = B f0 on stream s.  st != nullptr: every kernel exits at entry once the solve is done.
 // rho != nullptr: level-0 post-sweep (or the direct solve) also reduces (z0, f0) into rho's control.
@@ -392,7 +417,7 @@ long long enqueue_vcycle(ldu_handle h, const double* f0, double* z0, cudaStream_
     const double* f = l ? Lv.f : f0;
     if (l == 0) {
       with_format(h, [&](auto A) {
-        k_vc_pre<<<h->gridA, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f, Lv.r, st);
+        k_vc_pre<<<H->gPre, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f, Lv.r, st);
       });
     } else {
       launch_csr(Lv.A, EpiPre{Lv.x, f, Lv.r}, st, s);
@@ -424,10 +449,10 @@ long long enqueue_vcycle(ldu_handle h, const double* f0, double* z0, cudaStream_
       launch_csr(Lv.P, EpiProlong0{Lv.omega, Lv.rD, f, xc, Lv.x}, st, s);
       with_format(h, [&](auto A) {
         if (rho)
-          k_vc_post<decltype(A), true><<<h->gridA, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f,
+          k_vc_post<decltype(A), true><<<H->gPost, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f,
                                                                    Lv.x, z0, st, *rho);
         else
-          k_vc_post<decltype(A), false><<<h->gridA, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f,
+          k_vc_post<decltype(A), false><<<H->gPost, kBlock, 0, s>>>(A, Lv.diag, Lv.rD, Lv.omega, f,
                                                                     Lv.x, z0, st, Red{});
       });
     } else {
@@ -473,7 +498,7 @@ long long enqueue_amg_iters_mr(ldu_handle h, bool pipelined, int batch, cudaStre
   for (int it = 0; it < batch; ++it) {
     prof_mark(h, profile, 4 * it + 0, s);
     if (!pipelined) {
-      const Red rr = red_of(h, CTL_NONE, false, H->L ? h->gridA : h->grid);
+      const Red rr = red_of(h, CTL_NONE, false, H->L ? H->gPost : h->grid);
       kernels += enqueue_vcycle(h, h->r, H->zk, s, h->st, &rr);
       prof_mark(h, profile, 4 * it + 1, s);
       allgather_ctl(h, CTL_AMG_RHO, 1, s, kernels);
@@ -515,13 +540,13 @@ long long enqueue_amg_iters(ldu_handle h, bool pipelined, int batch, cudaStream_
   for (int it = 0; it < batch; ++it) {
     prof_mark(h, profile, 4 * it + 0, s);
     if (!pipelined) {
-      const Red rr = red_of(h, CTL_AMG_RHO, true, H->L ? h->gridA : h->grid);
+      const Red rr = red_of(h, CTL_AMG_RHO, true, H->L ? H->gPost : h->grid);
       kernels += enqueue_vcycle(h, h->r, H->zk, s, h->st, &rr);
       prof_mark(h, profile, 4 * it + 1, s);
       prof_mark(h, profile, 4 * it + 2, s);
       with_format(h, [&](auto A) {
-        k_amg_passA<<<h->gridA, kBlock, 0, s>>>(A, h->diag, H->zk, h->p0, h->p1, h->q, h->x,
-                                                h->st, red_of(h, CTL_CG_A, true, h->gridA));
+        k_amg_passA<<<H->gPassA, kBlock, 0, s>>>(A, h->diag, H->zk, h->p0, h->p1, h->q, h->x,
+                                                 h->st, red_of(h, CTL_CG_A, true, H->gPassA));
       });
       k_amg_passB<<<h->grid, kBlock, 0, s>>>(h->n, h->q, h->r, h->st, red_of(h, CTL_AMG_B, true));
       kernels += 2;
@@ -530,9 +555,9 @@ long long enqueue_amg_iters(ldu_handle h, bool pipelined, int batch, cudaStream_
       prof_mark(h, profile, 4 * it + 1, s);
       prof_mark(h, profile, 4 * it + 2, s);
       with_format(h, [&](auto A) {
-        k_amg_pipe_SU<<<h->gridA, kBlock, 0, s>>>(A, h->diag, H->m, h->z, H->qk, h->s, h->p0, h->x,
+        k_amg_pipe_SU<<<H->gPipe, kBlock, 0, s>>>(A, h->diag, H->m, h->z, H->qk, h->s, h->p0, h->x,
                                                   h->r, H->u, h->w, h->st,
-                                                  red_of(h, CTL_PIPE_NEXT, true, h->gridA));
+                                                  red_of(h, CTL_PIPE_NEXT, true, H->gPipe));
       });
       ++kernels;
     }
@@ -548,6 +573,7 @@ long long enqueue_amg_iters(ldu_handle h, bool pipelined, int batch, cudaStream_
 // ---------------------------------------------------------------------------------------------
 void amg_vcycle(ldu_handle h, const double* r, double* z) {
   if (!h->amg) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+  amg_grids(h);
   if (!r || !z) fail_arg("r and z must not be NULL");
   cudaStream_t s = h->own_stream;
   h->stats = ldu_solve_stats{};
@@ -610,6 +636,7 @@ ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, d
   const int batch = o.batch ? o.batch : 8;
 
   ensure_amg_work(h, pipelined);
+  amg_grids(h);
   const int n = h->n;
   const bool mr = multi(h);
   if (mr && pipelined) ensure_vec(h->nv, n);

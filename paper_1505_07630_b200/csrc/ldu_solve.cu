@@ -1952,6 +1952,9 @@ void configure(ldu_handle h) {
     });
   }
   if (use_tma(h)) h->gridA = h->tGrid;
+  if (h->variant == 7) {  // the SpMV-bearing kernel of the split pass A is k_cg_passA2 (40 regs)
+    with_format(h, [&](auto A) { h->gridA = grid_of((const void*)k_cg_passA2<decltype(A)>); });
+  }
   // fused pipelined pass: 6 resident blocks per SM (LDU_SU_MINB=8 single rank: 8, measured slower)
   h->suMinB = 6;
   if (const char* v = std::getenv("LDU_SU_MINB")) h->suMinB = std::atoi(v) == 8 && !(h->comm && h->comm->nRanks > 1) ? 8 : 6;
