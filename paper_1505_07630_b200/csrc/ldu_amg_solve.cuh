@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kBlock) k_amg_dot(int n, const double* __restr
 
 // ---- Krylov passes ----------------------------------------------------------------------------
 template <class Fmt>
-__global__ void __launch_bounds__(kBlock) k_amg_passA(Fmt A, const double* __restrict__ diag,
+__global__ void __launch_bounds__(kBlock, 8) k_amg_passA(Fmt A, const double* __restrict__ diag,
                                                       const double* __restrict__ z, double* p0,
                                                       double* p1, double* __restrict__ q,
                                                       double* __restrict__ x, State* st, Red rd) {

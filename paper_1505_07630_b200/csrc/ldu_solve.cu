@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_passA1(int n, const double* __res
 }
 
 template <class Fmt>
-__global__ void __launch_bounds__(kBlock) k_cg_passA2(Fmt A, const double* __restrict__ rD,
+__global__ void __launch_bounds__(kBlock, 8) k_cg_passA2(Fmt A, const double* __restrict__ rD,
                                                       const double* p0, const double* p1,
                                                       double* __restrict__ q, State* st, Red rd) {
   if (st->done) return;
