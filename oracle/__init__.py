@@ -55,6 +55,8 @@ def _load():
         lib.oracle_pcg.restype = I
         lib.oracle_pipecg.argtypes = [I, I, P, P, P, P, P, P, P, D, I, I, I, P, P, P, D, I]
         lib.oracle_pipecg.restype = I
+        lib.oracle_pipecg_rr.argtypes = [I, I, P, P, P, P, P, P, P, D, I, I, I, P, P, P, D, I, I]
+        lib.oracle_pipecg_rr.restype = I
         _lib = lib
     return _lib
 
@@ -134,8 +136,9 @@ def pcg(sys, b: np.ndarray, x0: Optional[np.ndarray] = None, tol: float = 1e-10,
 
 def pipecg(sys, b: np.ndarray, x0: Optional[np.ndarray] = None, tol: float = 1e-10,
            maxIter: int = 10000, norm: int = NORM_L2, mode: int = JACOBI, history: bool = False,
-           relTol: float = 0.0, minIter: int = 0):
-    """Ghysels-Vanroose pipelined CG (mode LITERAL or JACOBI).  Returns like ``pcg``."""
+           relTol: float = 0.0, minIter: int = 0, replace_every: int = 0):
+    """Ghysels-Vanroose pipelined CG (mode LITERAL or JACOBI), optionally with residual
+    replacement every ``replace_every`` iterations (NEXT-4).  Returns like ``pcg``."""
     lib = _load()
     l, u, d, lo, up = _arrays(sys)
     bb = np.ascontiguousarray(b, dtype=np.float64)
@@ -143,9 +146,14 @@ def pipecg(sys, b: np.ndarray, x0: Optional[np.ndarray] = None, tol: float = 1e-
     it = ctypes.c_int(0)
     res = ctypes.c_double(0.0)
     hist = np.full(maxIter + 1, np.nan) if history else None
-    st = lib.oracle_pipecg(sys.nCells, l.shape[0], _p(l), _p(u), _p(d), _p(lo), _p(up), _p(bb),
-                           _p(x), tol, maxIter, norm, mode, ctypes.byref(it), ctypes.byref(res),
-                           _p(hist), relTol, minIter)
+    if replace_every:
+        st = lib.oracle_pipecg_rr(sys.nCells, l.shape[0], _p(l), _p(u), _p(d), _p(lo), _p(up),
+                                  _p(bb), _p(x), tol, maxIter, norm, mode, ctypes.byref(it),
+                                  ctypes.byref(res), _p(hist), relTol, minIter, int(replace_every))
+    else:
+        st = lib.oracle_pipecg(sys.nCells, l.shape[0], _p(l), _p(u), _p(d), _p(lo), _p(up),
+                               _p(bb), _p(x), tol, maxIter, norm, mode, ctypes.byref(it),
+                               ctypes.byref(res), _p(hist), relTol, minIter)
     if history:
         return st, x, it.value, res.value, hist[: it.value + 1]
     return st, x, it.value, res.value

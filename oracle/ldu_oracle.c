@@ -207,10 +207,15 @@ int oracle_pcg(int n, int nf, const int *l, const int *u, const double *diag,
 
 /* ---- pipelined CG, Ghysels & Vanroose Alg. 4 with M = diag ------------- */
 
+/* replaceEvery > 0 (NEXT-4, residual replacement; Ghysels & Vanroose 2014, Sec. 4 [ext]): after
+ * the updates of every iteration i with (i + 1) % replaceEvery == 0 the recurrence vectors are
+ * recomputed from their definitions -- r = b - A x, u = M r, w = A u, s = A p, q = M s,
+ * z = A q -- before the next fused reduction.  Equal iterates in exact arithmetic. */
 static int pipecg_core(int n, int nf, const int *l, const int *u, const double *diag,
                        const double *lower, const double *upper, const double *b, double *x,
                        double tol, int maxIter, int norm, int mode, int *nIter, double *finalRes,
-                       double *hist, double relTol, int minIter, const prec_t *M)
+                       double *hist, double relTol, int minIter, const prec_t *M,
+                       int replaceEvery)
 {
     if (n <= 0 || nf < 0 || maxIter < 0 || !b || !x || !diag || (mode != 0 && mode != 1) ||
         relTol < 0 || minIter < 0 || (M && mode != 0))
@@ -287,6 +292,17 @@ static int pipecg_core(int n, int nf, const int *l, const int *u, const double *
         }
         gamma_old = gamma;
         alpha_old = alpha;
+        if (replaceEvery > 0 && (i + 1) % replaceEvery == 0) {   /* residual replacement */
+            amul(&A, x, nn);
+            for (int c = 0; c < n; ++c) r[c] = b[c] - nn[c];        /* r = b - A x          */
+            if (M) M->apply(M->ctx, r, uu);                          /* u = M r              */
+            else for (int c = 0; c < n; ++c) uu[c] = rD[c] * r[c];
+            amul(&A, uu, w);                                         /* w = A u              */
+            amul(&A, p, s);                                          /* s = A p              */
+            if (M) M->apply(M->ctx, s, q);                           /* q = M s              */
+            else for (int c = 0; c < n; ++c) q[c] = rD[c] * s[c];
+            amul(&A, q, z);                                          /* z = A q              */
+        }
     }
 out:
     free(r); free(uu); free(w); free(m); free(nn); free(z); free(q); free(s); free(p); free(rD);
@@ -299,7 +315,18 @@ int oracle_pipecg(int n, int nf, const int *l, const int *u, const double *diag,
                   double *hist, double relTol, int minIter)
 {
     return pipecg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, mode, nIter,
-                       finalRes, hist, relTol, minIter, NULL);
+                       finalRes, hist, relTol, minIter, NULL, 0);
+}
+
+/* pipelined CG with residual replacement every replaceEvery iterations (NEXT-4) */
+int oracle_pipecg_rr(int n, int nf, const int *l, const int *u, const double *diag,
+                     const double *lower, const double *upper, const double *b, double *x,
+                     double tol, int maxIter, int norm, int mode, int *nIter, double *finalRes,
+                     double *hist, double relTol, int minIter, int replaceEvery)
+{
+    if (replaceEvery < 0) return OR_ERR_ARG;
+    return pipecg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, mode, nIter,
+                       finalRes, hist, relTol, minIter, NULL, replaceEvery);
 }
 
 /* ==== Aggregation AMG preconditioner (NEXT-2; Table 2) =====================
@@ -495,7 +522,7 @@ int oracle_amg_pcg(int n, int nf, const int *l, const int *u, const double *diag
     amg_t H = amg_unflatten(F, buf);
     prec_t M = {amg_apply, &H};
     int st = pipelined ? pipecg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, 0,
-                                     nIter, finalRes, hist, relTol, minIter, &M)
+                                     nIter, finalRes, hist, relTol, minIter, &M, 0)
                        : pcg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, nIter,
                                   finalRes, hist, relTol, minIter, &M);
     free(buf);
@@ -559,7 +586,7 @@ int oracle_amg_block_pcg(int n, int nf, const int *l, const int *u, const double
     amg_blocks_t B = {nb, start, H};
     prec_t M = {amg_blocks_apply, &B};
     int st = pipelined ? pipecg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, 0,
-                                     nIter, finalRes, hist, relTol, minIter, &M)
+                                     nIter, finalRes, hist, relTol, minIter, &M, 0)
                        : pcg_core(n, nf, l, u, diag, lower, upper, b, x, tol, maxIter, norm, nIter,
                                   finalRes, hist, relTol, minIter, &M);
     for (int g = 0; g < nb; ++g) free(bufs[g]);

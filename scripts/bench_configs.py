@@ -215,6 +215,27 @@ def c2amg(ldu):
                           "amg_levels": info["n"] if name == "amg_pcg" else None}), flush=True)
 
 
+def accuracy(ldu, sizes=(128, 256, 512)):
+    """NEXT-4's condition: is the attainable accuracy of plain Ghysels-Vanroose
+    pipelined CG (no residual replacement, reading Z7) a limit?  True residual ||b - A x|| / ||b||
+    (library SpMV) vs the recurrence residual at tight tolerances, both solvers, hot-face RHS."""
+    for n in sizes:
+        s = meshgen.hex_laplacian(n, n, n, dirichlet=dict(x0=1.0))
+        A = ldu.LduMatrix.from_system(s)
+        b = torch.from_numpy(s.b).cuda()
+        for tol in (1e-10, 1e-12, 1e-14):
+            for name, fn in (("pcg", A.pcg_solve), ("pipecg", A.pipecg_solve)):
+                x = torch.zeros_like(b)
+                st, it, res = fn(b, x, tol=tol, maxIter=20000)
+                y = torch.empty_like(x)
+                A.amul(x, y)
+                true = float(torch.linalg.norm(b - y) / torch.linalg.norm(b))
+                print(json.dumps({"config": f"accuracy {n}^3 hot face", "solver": name, "tol": tol,
+                                  "status": int(st), "iters": it, "recurrence_res": res,
+                                  "true_res": true}), flush=True)
+        A.close()
+
+
 def c4(ldu, iters=300):
     """512^3 z-slabs over N GPUs (torchrun), fixed iterations, both solvers."""
     import torch.distributed as dist
@@ -342,4 +363,4 @@ if __name__ == "__main__":
         c5dist(ldu, slow_rank_sms=int(sys.argv[2]) if len(sys.argv) > 2 else 40)
     else:
         {"c1": c1, "c2": c2, "c4": c4, "c5": c5, "c5dist": c5dist, "c5amg": c5amg,
-         "c2amg": c2amg}[which](ldu)
+         "c2amg": c2amg, "accuracy": accuracy}[which](ldu)

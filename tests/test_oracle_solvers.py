@@ -271,3 +271,34 @@ def test_reltol_and_miniter(solver):
     st, x, it, res = f(sys, b, tol=1e300, maxIter=200, minIter=7)
     _, x7, it7, _ = f(sys, b, tol=0.0, maxIter=7)
     assert st == oracle.OK and it == 7 and np.array_equal(x, x7)
+
+
+# ---- residual replacement in pipelined CG (NEXT-4) ------------------------------------------------
+def _true_res(s, b, x):
+    return np.linalg.norm(b - oracle.amul(s, x)) / np.linalg.norm(b)
+
+
+def test_pipecg_replacement_identical_until_first_replacement():
+    s = meshgen.hex_laplacian(20, 20, 20, dirichlet=dict(x0=1.0))
+    _, _, _, _, h0 = oracle.pipecg(s, s.b, tol=0.0, maxIter=40, history=True)
+    _, _, _, _, h1 = oracle.pipecg(s, s.b, tol=0.0, maxIter=40, history=True, replace_every=25)
+    np.testing.assert_array_equal(h0[:25], h1[:25])  # residuals 0..24: the first replacement follows update 24
+    assert np.allclose(h0[25:], h1[25:], rtol=1e-6)   # equal in exact arithmetic
+
+
+def test_pipecg_replacement_restores_attainable_accuracy():
+    """Plain Ghysels-Vanroose CG drifts: at 64^3 its true residual stalls above tol and at
+    tol 1e-14 the recurrences break down; with the residual recomputed every 50 iterations the
+    TRUE residual meets the tolerance in classical CG's iteration count (the methods coincide in
+    exact arithmetic)."""
+    s = meshgen.hex_laplacian(64, 64, 64, dirichlet=dict(x0=1.0))
+    b = s.b
+    st, x, it, res = oracle.pipecg(s, b, tol=1e-12, maxIter=3000)
+    assert st == oracle.OK and _true_res(s, b, x) > 2e-12            # recurrence says < 1e-12
+    st, x, it, res = oracle.pipecg(s, b, tol=1e-12, maxIter=3000, replace_every=50)
+    assert st == oracle.OK and _true_res(s, b, x) < 1e-12
+    _, _, it_cg, _ = oracle.pcg(s, b, tol=1e-14, maxIter=3000)
+    st0, _, _, _ = oracle.pipecg(s, b, tol=1e-14, maxIter=3000)
+    assert st0 == oracle.BREAKDOWN
+    st, x, it, res = oracle.pipecg(s, b, tol=1e-14, maxIter=3000, replace_every=50)
+    assert st == oracle.OK and abs(it - it_cg) <= 2 and _true_res(s, b, x) < 1.1e-14
