@@ -144,7 +144,9 @@ typedef struct {
                         per-pass device time in ldu_solve_stats.passMs (one host sync per batch) */
   int minIter;       /* OpenFOAM minIter: the stopping test cannot pass before minIter x-updates
                         (maxIter still ends the solve, NOT_CONVERGED; reading Z26)            */
-  int reserved;      /* must be zero                                                            */
+  int replaceEvery;  /* pipelined CG only (NEXT-4): > 0 recomputes r = b - A x, w = A M r, s = A p,
+                        z = A M s from their definitions after every replaceEvery-th iteration
+                        (residual replacement, attainable accuracy); 0 = off.  Single rank.    */
   double relTol;     /* OpenFOAM relTol: also converged when res < relTol * res0 (0 = off, Z26)  */
   double reserved2[2]; /* must be zero                                                          */
 } ldu_solve_opts;

@@ -51,7 +51,7 @@ class _Interfaces(ctypes.Structure):
 
 class SolveOpts(ctypes.Structure):
     _fields_ = [("norm", ctypes.c_int), ("recordHistory", ctypes.c_int), ("batch", ctypes.c_int),
-                ("profile", ctypes.c_int), ("minIter", ctypes.c_int), ("reserved", ctypes.c_int),
+                ("profile", ctypes.c_int), ("minIter", ctypes.c_int), ("replaceEvery", ctypes.c_int),
                 ("relTol", ctypes.c_double), ("reserved2", ctypes.c_double * 2)]
 
 
@@ -253,11 +253,11 @@ class LduMatrix:
         return y
 
     def _solve(self, fn, b, x, tol, maxIter, norm, record_history, batch, profile=False,
-               relTol=0.0, minIter=0):
+               relTol=0.0, minIter=0, replaceEvery=0):
         it = _I(0)
         res = _D(0.0)
         opts = SolveOpts(norm, 1 if record_history else 0, batch, 1 if profile else 0,
-                         int(minIter), 0, float(relTol))
+                         int(minIter), int(replaceEvery), float(relTol))
         st = fn(self.handle, _ptr(b, "f64"), _ptr(x, "f64"), float(tol), int(maxIter),
                 ctypes.byref(opts), ctypes.byref(it), ctypes.byref(res))
         if st < 0:
@@ -266,17 +266,19 @@ class LduMatrix:
 
     def pcg_solve(self, b, x, tol: float = 1e-10, maxIter: int = 10000, norm: int = NORM_L2,
                   record_history: bool = False, batch: int = 0, profile: bool = False,
-                  relTol: float = 0.0, minIter: int = 0):
-        """Jacobi-PCG; x is in/out.  Returns (status, nIter, finalRes)."""
+                  relTol: float = 0.0, minIter: int = 0, replaceEvery: int = 0):
+        """Jacobi-PCG; x is in/out.  Returns (status, nIter, finalRes).  (replaceEvery is passed
+        through to the C ABI, which rejects it: residual replacement is pipelined-only.)"""
         return self._solve(_lib.pcg_solve_ex, b, x, tol, maxIter, norm, record_history, batch,
-                           profile, relTol, minIter)
+                           profile, relTol, minIter, replaceEvery)
 
     def pipecg_solve(self, b, x, tol: float = 1e-10, maxIter: int = 10000, norm: int = NORM_L2,
                      record_history: bool = False, batch: int = 0, profile: bool = False,
-                     relTol: float = 0.0, minIter: int = 0):
-        """Ghysels-Vanroose pipelined CG; x is in/out.  Returns (status, nIter, finalRes)."""
+                     relTol: float = 0.0, minIter: int = 0, replaceEvery: int = 0):
+        """Ghysels-Vanroose pipelined CG; x is in/out; replaceEvery > 0 recomputes the recurrence
+        vectors every replaceEvery iterations (NEXT-4).  Returns (status, nIter, finalRes)."""
         return self._solve(_lib.pipecg_solve_ex, b, x, tol, maxIter, norm, record_history, batch,
-                           profile, relTol, minIter)
+                           profile, relTol, minIter, replaceEvery)
 
     # -- aggregation-AMG preconditioner (NEXT-2, P:236) --------------------------------------
     def amg_setup(self, coarsest: int = 0, maxLevels: int = 0, keyIndexOrder: bool = False,

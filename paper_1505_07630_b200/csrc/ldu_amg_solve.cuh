@@ -624,8 +624,9 @@ ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, d
   ldu_solve_opts o{};
   if (opts) {
     o = *opts;
-    if (o.reserved || o.reserved2[0] != 0.0 || o.reserved2[1] != 0.0)
-      fail_arg("ldu_solve_opts.reserved must be zero");
+    if (o.replaceEvery) fail_arg("replaceEvery is not supported by the AMG solvers");
+    if (o.reserved2[0] != 0.0 || o.reserved2[1] != 0.0)
+      fail_arg("ldu_solve_opts.reserved2 must be zero");
   }
   if (!(o.relTol >= 0.0)) fail_arg("relTol must be >= 0");
   if (o.minIter < 0) fail_arg("minIter must be >= 0");

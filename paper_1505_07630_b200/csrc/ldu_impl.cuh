@@ -177,6 +177,7 @@ struct ldu_handle_s {
     long long kernels = 0;  // kernels per captured batch
   };
   Graph graphs[2][2];       // [pipelined][profile]
+  Graph graphRR[2];         // pipelined with residual replacement, [profile]
   std::vector<cudaEvent_t> prof_ev;  // profile mode: 4 events per iteration of a batch
   std::vector<cudaEvent_t> trace;    // LDU_TRACE debug events
   // interfaces

@@ -1251,6 +1251,85 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
   return kernels;
 }
 
+// ---- residual replacement in the single-rank fused pipelined loop (NEXT-4) --------------------
+// y = A x including the diagonal, skipped once the solve is done
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_amul_st(Fmt A, const double* __restrict__ diag,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y, const State* st) {
+  if (st->done) return;
+  GRID_STRIDE(c, A.n) {
+    y[c] = row_apply(A, c, __ldg(diag + c) * __ldg(x + c), [&](int j) { return __ldg(x + j); });
+  }
+}
+
+// r = b - A x
+__global__ void __launch_bounds__(kBlock) k_rr_r(int n, const double* __restrict__ b,
+                                                 const double* __restrict__ ax,
+                                                 double* __restrict__ r, const State* st) {
+  if (st->done) return;
+  GRID_STRIDE(c, n) r[c] = b[c] - ax[c];
+}
+
+// w_{i+1} = A (rD . r) into the ping-pong half the next fused pass reads (k not yet advanced)
+template <class Fmt>
+__global__ void __launch_bounds__(kBlock) k_rr_w(Fmt A, const double* __restrict__ rD,
+                                                 const double* __restrict__ r, double* w0,
+                                                 double* w1, const State* st) {
+  if (st->done) return;
+  double* __restrict__ wn = (st->k & 1) ? w0 : w1;
+  GRID_STRIDE(c, A.n) {
+    wn[c] = row_apply(A, c, __ldg(r + c), [&](int j) { return __ldg(rD + j) * __ldg(r + j); });
+  }
+}
+
+// the iteration's fused reduction over the replaced vectors: [(r, rD.r), (w, rD.r), crit(r)]
+__global__ void __launch_bounds__(kBlock) k_rr_dots(int n, const double* __restrict__ rD,
+                                                    const double* __restrict__ r, const double* w0,
+                                                    const double* w1, State* st, Red rd) {
+  if (st->done) return;
+  const double* __restrict__ w = (st->k & 1) ? w0 : w1;
+  const bool l2 = st->norm == LDU_NORM_L2;
+  double v[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(c, n) {
+    const double rc = r[c], u = rD[c] * rc;
+    v[0] = fma(rc, u, v[0]);
+    v[1] = fma(w[c], u, v[1]);
+    v[2] += l2 ? rc * rc : fabs(rc);
+  }
+  finish_reduction<3>(v, rd, st);
+}
+
+// One batch of `batch` fused pipelined iterations whose last one is followed by the residual
+// replacement: its fused pass reduces without the control step, the vectors are recomputed from
+// their definitions (r = b - A x, w = A rD r, s = A p, z = A rD s; Jacobi form of GV Sec. 4), and
+// the reduction of the replaced vectors runs the control step of the next iteration.
+long long enqueue_pipe_rr(ldu_handle h, int batch, cudaStream_t s, bool profile) {
+  long long kernels = 0;
+  for (int it = 0; it < batch; ++it) {
+    const bool last = it == batch - 1;
+    prof_mark(h, profile, 4 * it + 0, s);
+    prof_mark(h, profile, 4 * it + 1, s);
+    prof_mark(h, profile, 4 * it + 2, s);
+    with_format(h, [&](auto A) {
+      k_pipe_SU<<<h->gridSU, kBlock, 0, s>>>(A, h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x, h->r,
+                                              h->st, red_of(h, last ? CTL_NONE : CTL_PIPE_NEXT, true, h->gridSU));
+    });
+    prof_mark(h, profile, 4 * it + 3, s);
+    ++kernels;
+  }
+  with_format(h, [&](auto A) {
+    k_amul_st<<<h->gridA, kBlock, 0, s>>>(A, h->diag, h->x, h->ybuf, h->st);
+    k_rr_r<<<h->grid, kBlock, 0, s>>>(h->n, h->bbuf, h->ybuf, h->r, h->st);
+    k_rr_w<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->r, h->w, h->w2, h->st);
+    k_amul_st<<<h->gridA, kBlock, 0, s>>>(A, h->diag, h->p0, h->s, h->st);
+    k_spmv_scaled<<<h->gridA, kBlock, 0, s>>>(A, h->rD, h->s, h->z, h->st);
+  });
+  k_rr_dots<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->r, h->w, h->w2, h->st,
+                                       red_of(h, CTL_PIPE_NEXT, true));
+  return kernels + 6;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
@@ -1299,16 +1378,21 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   ldu_solve_opts o{};
   if (opts) {
     o = *opts;
-    if (o.reserved || o.reserved2[0] != 0.0 || o.reserved2[1] != 0.0)
-      fail_arg("ldu_solve_opts.reserved must be zero");
+    if (o.reserved2[0] != 0.0 || o.reserved2[1] != 0.0)
+      fail_arg("ldu_solve_opts.reserved2 must be zero");
   }
   if (!(o.relTol >= 0.0)) fail_arg("relTol must be >= 0");
   if (o.minIter < 0) fail_arg("minIter must be >= 0");
   if (o.norm != LDU_NORM_L2 && o.norm != LDU_NORM_OPENFOAM) fail_arg("unknown norm");
   if (o.batch < 0) fail_arg("batch must be >= 0");
   if (o.profile != 0 && o.profile != 1) fail_arg("profile must be 0 or 1");
+  if (o.replaceEvery < 0) fail_arg("replaceEvery must be >= 0");
+  const int rr = o.replaceEvery;
+  if (rr && !pipelined) fail_arg("replaceEvery applies to pipelined CG only");
+  if (rr && (multi(h) || !h->fusePipe))
+    throw Error(LDU_ERR_STATE, "residual replacement needs the single-rank fused pipelined pass");
   const bool profile = o.profile == 1;
-  const int batch = o.batch ? o.batch : 32;
+  const int batch = rr ? rr : (o.batch ? o.batch : 32);
 
   ensure_work(h, pipelined);
   const int n = h->n;
@@ -1335,6 +1419,11 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   }
   CUDA_CHECK(cudaMemcpyAsync(h->x, x, sizeof(double) * n, xd ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   if (!xd) h->stats.h2dBytes += 8LL * n;
+  if (rr && bin != h->bbuf) {  // the replacement graph reads b from a fixed buffer
+    ensure_vec(h->bbuf, n);
+    CUDA_CHECK(cudaMemcpyAsync(h->bbuf, bin, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    bin = h->bbuf;
+  }
 
   // history buffer
   if (o.recordHistory) {
@@ -1420,7 +1509,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   CUDA_CHECK(cudaEventRecord(h->ev[1], s));
 
   // ---- single rank, persistent cooperative kernel (latency-bound sizes) --------------------
-  if (!mr && h->persist) {
+  if (!mr && h->persist && !rr) {
     if (!h->ppartials) h->ppartials = dmalloc<double>((size_t)2 * kMaxVals * h->gridP);
     CUDA_CHECK(cudaEventRecord(h->ev[1], s));
     long long launches = 0;
@@ -1497,13 +1586,14 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   }
 
   // ---- iteration batches as CUDA graphs ----------------------------------------------------
-  ldu_handle_s::Graph& G = h->graphs[pipelined ? 1 : 0][profile ? 1 : 0];
+  ldu_handle_s::Graph& G = rr ? h->graphRR[profile ? 1 : 0] : h->graphs[pipelined ? 1 : 0][profile ? 1 : 0];
   if (profile && (int)h->prof_ev.size() < 4 * batch) {
     for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
     h->prof_ev.assign(4 * batch, nullptr);
     for (auto& e : h->prof_ev) CUDA_CHECK(cudaEventCreate(&e));
     if (h->graphs[0][1].exec) { cudaGraphExecDestroy(h->graphs[0][1].exec); h->graphs[0][1] = {}; }
     if (h->graphs[1][1].exec) { cudaGraphExecDestroy(h->graphs[1][1].exec); h->graphs[1][1] = {}; }
+    if (h->graphRR[1].exec) { cudaGraphExecDestroy(h->graphRR[1].exec); h->graphRR[1] = {}; }
   }
   if (const char* tr = std::getenv("LDU_TRACE"); tr && std::atoi(tr) == 1 && (int)h->trace.size() < 5 * batch) {
     h->trace.assign(5 * batch, nullptr);
@@ -1511,6 +1601,8 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     for (auto& row : h->graphs)
       for (auto& GG : row)
         if (GG.exec) { cudaGraphExecDestroy(GG.exec); GG = {}; }
+    for (auto& GG : h->graphRR)
+      if (GG.exec) { cudaGraphExecDestroy(GG.exec); GG = {}; }
   }
   if (!G.exec || G.batch != batch) {
     if (G.exec) {
@@ -1520,8 +1612,9 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     const ldu_solve_stats saved = h->stats;  // capture enqueues nothing that runs now
     cudaGraph_t g;
     CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    G.kernels = pipelined ? enqueue_pipe_iters(h, batch, s, profile)
-                          : enqueue_cg_iters(h, batch, s, profile);
+    G.kernels = rr ? enqueue_pipe_rr(h, batch, s, profile)
+                   : pipelined ? enqueue_pipe_iters(h, batch, s, profile)
+                               : enqueue_cg_iters(h, batch, s, profile);
     CUDA_CHECK(cudaStreamEndCapture(s, &g));
     CUDA_CHECK(cudaGraphInstantiate(&G.exec, g, 0));
     CUDA_CHECK(cudaGraphDestroy(g));
@@ -1674,6 +1767,10 @@ void release_work(ldu_handle h) {
       if (G.exec) cudaGraphExecDestroy(G.exec);
       G = {};
     }
+  for (auto& G : h->graphRR) {
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    G = {};
+  }
   for (cudaEvent_t e : h->prof_ev) cudaEventDestroy(e);
   h->prof_ev.clear();
 }

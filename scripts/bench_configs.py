@@ -224,15 +224,20 @@ def accuracy(ldu, sizes=(128, 256, 512)):
         A = ldu.LduMatrix.from_system(s)
         b = torch.from_numpy(s.b).cuda()
         for tol in (1e-10, 1e-12, 1e-14):
-            for name, fn in (("pcg", A.pcg_solve), ("pipecg", A.pipecg_solve)):
+            for name, fn, kw in (("pcg", A.pcg_solve, {}), ("pipecg", A.pipecg_solve, {}),
+                                 ("pipecg_rr50", A.pipecg_solve, {"replaceEvery": 50})):
                 x = torch.zeros_like(b)
-                st, it, res = fn(b, x, tol=tol, maxIter=20000)
+                fn(b, x, tol=tol, maxIter=20000, **kw)
+                x = torch.zeros_like(b)
+                st, it, res = fn(b, x, tol=tol, maxIter=20000, **kw)
+                ms = A.stats()["solveMs"]
                 y = torch.empty_like(x)
                 A.amul(x, y)
                 true = float(torch.linalg.norm(b - y) / torch.linalg.norm(b))
                 print(json.dumps({"config": f"accuracy {n}^3 hot face", "solver": name, "tol": tol,
                                   "status": int(st), "iters": it, "recurrence_res": res,
-                                  "true_res": true}), flush=True)
+                                  "true_res": true, "solve_ms": ms,
+                                  "ms_per_iter": ms / max(1, it)}), flush=True)
         A.close()
 
 

@@ -296,3 +296,59 @@ def test_reltol_miniter_parity(ldu, solver):
             st, it, res = fn(b, x, maxIter=maxIter, norm=ldu.NORM_OPENFOAM, **kw)
             assert st == ost and it == oit, (kw, st, ost, it, oit)
             assert rel(x, ox) <= 1e-10
+
+
+# ---- residual replacement in pipelined CG (NEXT-4) ------------------------------------------------
+def test_pipecg_replacement_parity(ldu):
+    """replaceEvery = 25 on the device = the oracle's pipelined CG with the same replacement
+    (counts, solution, residual history across two replacements) -- fixed and to tolerance."""
+    s = meshgen.hex_laplacian(24, 24, 24, conductance_sigma=0.3, seed=4, dirichlet=dict(x0=1.0))
+    ost, ox, oit, ores, ohist = oracle.pipecg(s, s.b, tol=1e-10, maxIter=2000, history=True,
+                                              replace_every=25)
+    with ldu.LduMatrix.from_system(s) as A:
+        x = torch.zeros(s.nCells, dtype=torch.float64, device="cuda")
+        st, it, res = A.pipecg_solve(cuda(s.b), x, tol=1e-10, maxIter=2000, record_history=True,
+                                     replaceEvery=25)
+        hist = A.history()
+        assert st == ldu.OK and ost == oracle.OK and abs(it - oit) <= 1, (it, oit)
+        assert rel(x.cpu().numpy(), ox) <= 1e-8
+        np.testing.assert_allclose(hist[:60], ohist[:60], rtol=1e-8)
+        fst, fox, foit, fores, fohist = oracle.pipecg(s, s.b, tol=0.0, maxIter=60, history=True,
+                                                      replace_every=25)
+        x = torch.zeros(s.nCells, dtype=torch.float64, device="cuda")
+        st, it, res = A.pipecg_solve(cuda(s.b), x, tol=0.0, maxIter=60, record_history=True,
+                                     replaceEvery=25)
+        assert st == fst == ldu.NOT_CONVERGED and it == foit == 60
+        np.testing.assert_allclose(A.history(), fohist, rtol=1e-8)
+        assert rel(x.cpu().numpy(), fox) <= 1e-9
+        with pytest.raises(ldu.LduError) as e:
+            A.pcg_solve(cuda(s.b), x, tol=1e-8, maxIter=10, replaceEvery=5)
+        assert e.value.status == ldu.ERR_INVALID_ARG
+
+
+def test_pipecg_replacement_restores_attainable_accuracy(ldu):
+    """On the device, as in the oracle pin: plain GV pipelined CG at 64^3 stalls (true residual
+    above tol 1e-12) and breaks down at tol 1e-14; with replacement every 50 iterations the TRUE
+    residual (library SpMV) meets the tolerance in the classical iteration count."""
+    s = meshgen.hex_laplacian(64, 64, 64, dirichlet=dict(x0=1.0))
+    with ldu.LduMatrix.from_system(s) as A:
+        b = cuda(s.b)
+
+        def true_res(x):
+            y = torch.empty_like(x)
+            A.amul(x, y)
+            return (torch.linalg.norm(b - y) / torch.linalg.norm(b)).item()
+        x = torch.zeros_like(b)
+        st, it, res = A.pipecg_solve(b, x, tol=1e-12, maxIter=3000)
+        assert st == ldu.OK and true_res(x) > 2e-12
+        x = torch.zeros_like(b)
+        st, it, res = A.pipecg_solve(b, x, tol=1e-12, maxIter=3000, replaceEvery=50)
+        assert st == ldu.OK and true_res(x) < 1e-12
+        x = torch.zeros_like(b)
+        st0, _, _ = A.pipecg_solve(b, x, tol=1e-14, maxIter=3000)
+        assert st0 == ldu.BREAKDOWN
+        x = torch.zeros_like(b)
+        _, it_cg, _ = A.pcg_solve(b, x, tol=1e-14, maxIter=3000)
+        x = torch.zeros_like(b)
+        st, it, res = A.pipecg_solve(b, x, tol=1e-14, maxIter=3000, replaceEvery=50)
+        assert st == ldu.OK and abs(it - it_cg) <= 2 and true_res(x) < 1.1e-14
