@@ -5,6 +5,7 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
 ``-O2 -ffp-contract=off``, single thread) through ctypes and shares no code with the CUDA library
 ``paper_1505_07630_b200``.  See ``ldu_oracle.c`` for the passage each function follows and the
 pins that hold it; DESIGN.md lists the readings Z1..Z33 of the paper it relies on.
+``dic`` / ``dic_pcg`` add OpenFOAM's DIC preconditioner (NEXT-1; readings Z35-Z36).
 ``oracle.amg`` adds the aggregation-AMG preconditioner of P:236 (NEXT-2; readings Z27-Z33).
 
 Parity status: every function here is pinned by ``tests/test_oracle_*.py`` (no "parity unpinned"
@@ -57,6 +58,10 @@ def _load():
         lib.oracle_pipecg.restype = I
         lib.oracle_pipecg_rr.argtypes = [I, I, P, P, P, P, P, P, P, D, I, I, I, P, P, P, D, I, I]
         lib.oracle_pipecg_rr.restype = I
+        lib.oracle_dic.argtypes = [I, I, P, P, P, P, I, P, P, P, P]
+        lib.oracle_dic.restype = I
+        lib.oracle_dic_pcg.argtypes = [I, I, P, P, P, P, P, P, D, I, I, P, P, P, D, I, I, P, I]
+        lib.oracle_dic_pcg.restype = I
         _lib = lib
     return _lib
 
@@ -157,3 +162,54 @@ def pipecg(sys, b: np.ndarray, x0: Optional[np.ndarray] = None, tol: float = 1e-
     if history:
         return st, x, it.value, res.value, hist[: it.value + 1]
     return st, x, it.value, res.value
+
+
+# ---- DIC preconditioner (readings Z35, Z36) ----------------------------
+def _blocks_arg(sys, bounds):
+    if bounds is None:
+        return 1, None
+    st = np.ascontiguousarray(bounds, dtype=np.int32)
+    return st.shape[0] - 1, st
+
+
+def dic(sys, r: Optional[np.ndarray] = None, bounds: Optional[Sequence[int]] = None):
+    """OpenFOAM DIC: returns (status, rD, w) with rD the reciprocal D of
+    M = (D + L) D^-1 (D + L^T) and w = M^-1 r (None without r).  ``bounds`` = contiguous row
+    blocks (block-Jacobi DIC across ranks: faces joining two blocks dropped)."""
+    assert sys.lower is None or np.array_equal(sys.lower, sys.upper), "DIC needs a symmetric matrix"
+    lib = _load()
+    l, u, d, _, up = _arrays(sys)
+    nb, st = _blocks_arg(sys, bounds)
+    rD = np.empty(sys.nCells)
+    rr = None if r is None else np.ascontiguousarray(r, dtype=np.float64)
+    w = None if r is None else np.empty(sys.nCells)
+    status = lib.oracle_dic(sys.nCells, l.shape[0], _p(l), _p(u), _p(d), _p(up), nb, _p(st),
+                            _p(rD), _p(rr), _p(w))
+    if status < 0:
+        raise ValueError("oracle_dic: bad arguments")
+    return status, rD, w
+
+
+def dic_pcg(sys, b: np.ndarray, x0: Optional[np.ndarray] = None, tol: float = 1e-10,
+            maxIter: int = 10000, norm: int = NORM_L2, history: bool = False,
+            relTol: float = 0.0, minIter: int = 0, pipelined: bool = False,
+            bounds: Optional[Sequence[int]] = None):
+    """DIC-preconditioned CG (c2 with z = M^-1 r) or pipelined CG (c3 literal form).
+    Returns (status, x, nIter, finalRes[, hist])."""
+    assert sys.lower is None or np.array_equal(sys.lower, sys.upper), "DIC needs a symmetric matrix"
+    lib = _load()
+    l, u, d, _, up = _arrays(sys)
+    nb, st = _blocks_arg(sys, bounds)
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(sys.nCells) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    it = ctypes.c_int(0)
+    res = ctypes.c_double(0.0)
+    hist = np.full(maxIter + 1, np.nan) if history else None
+    status = lib.oracle_dic_pcg(sys.nCells, l.shape[0], _p(l), _p(u), _p(d), _p(up), _p(bb),
+                                _p(x), tol, maxIter, norm, ctypes.byref(it), ctypes.byref(res),
+                                _p(hist), relTol, minIter, nb, _p(st), 1 if pipelined else 0)
+    if status < 0:
+        raise ValueError("oracle_dic_pcg: bad arguments")
+    if history:
+        return status, x, it.value, res.value, hist[: it.value + 1]
+    return status, x, it.value, res.value

@@ -25,6 +25,9 @@
  *                    form (mode 0, u, q, m stored) and Jacobi-specialised form (mode 1, u = rD*r,
  *                    q = rD*s, m = rD*w never stored).  Pinned by iterate-wise equality with
  *                    oracle_pcg and the same solution pins.
+ *   oracle_dic,      OpenFOAM DIC preconditioner and DIC-(Pipe)CG (readings
+ *   oracle_dic_pcg   Z35-Z36).  Pinned by tests/test_oracle_dic.py: diag(M) = diag(A), IC(0) on
+ *                    hex meshes, exact Cholesky on a chain, dense M w = r, dense solves.
  */
 #include <math.h>
 #include <stdlib.h>
@@ -594,3 +597,121 @@ int oracle_amg_block_pcg(int n, int nf, const int *l, const int *u, const double
     return st;
 }
 
+
+/* ---- DIC preconditioner (OpenFOAM DICPreconditioner [ext]) -------------
+ * The default preconditioner of OpenFOAM's p solve (SURVEY NEXT-1 "Optional DIC preconditioner
+ * (OpenFOAM's default for p)"): diagonal-based incomplete Cholesky, M = (D + L) D^-1 (D + L^T),
+ * L = strictly-lower part of A, D chosen so that diag(M) = diag(A) (reading Z35).  Written as
+ * OpenFOAM's face loops over the faces in upper-triangular order (owner = min(l, u) ascending,
+ * then neighbour ascending; duplicate faces merged by summing, reading Z36):
+ *   calcReciprocalD:  rD = diag;  for f ascending:  rD[u_f] -= upper_f^2 / rD[l_f];  rD = 1/rD
+ *   precondition:     w = rD r;   for f ascending:  w[u_f] -= rD[u_f] upper_f w[l_f];
+ *                                 for f descending: w[l_f] -= rD[l_f] upper_f w[u_f]
+ * Block form (reading Z33 applied to DIC): with nb > 1 contiguous row blocks [start[g],
+ * start[g+1]), faces joining two blocks are dropped -- the multi-rank (processor-local) DIC.
+ * Symmetric matrices only (lower == NULL). */
+typedef struct { int nf; int *l, *u; double *a; double *rD; } dic_t;
+
+static const int *g_sort_l, *g_sort_u;
+static int cmp_face(const void *pa, const void *pb)
+{
+    int a = *(const int *)pa, b = *(const int *)pb;
+    int la = g_sort_l[a] < g_sort_u[a] ? g_sort_l[a] : g_sort_u[a];
+    int lb = g_sort_l[b] < g_sort_u[b] ? g_sort_l[b] : g_sort_u[b];
+    int ua = g_sort_l[a] < g_sort_u[a] ? g_sort_u[a] : g_sort_l[a];
+    int ub = g_sort_l[b] < g_sort_u[b] ? g_sort_u[b] : g_sort_l[b];
+    if (la != lb) return la < lb ? -1 : 1;
+    if (ua != ub) return ua < ub ? -1 : 1;
+    return a < b ? -1 : (a > b);
+}
+
+static int block_of(int nb, const int *start, int c)
+{
+    int g = 0;
+    while (g + 1 < nb && c >= start[g + 1]) ++g;
+    return g;
+}
+
+/* Builds the upper-triangular face list and rD; returns 0, or -1 (bad args) / -2 (pivot <= 0). */
+static int dic_make(int n, int nf, const int *l, const int *u, const double *diag,
+                    const double *upper, int nb, const int *start, dic_t *D)
+{
+    if (n <= 0 || nf < 0 || !diag || (nf && (!l || !u || !upper))) return -1;
+    if (nb < 1 || (nb > 1 && (!start || start[0] != 0 || start[nb] != n))) return -1;
+    int *ord = malloc(sizeof(int) * (size_t)(nf + 1));
+    for (int f = 0; f < nf; ++f) {
+        if (l[f] < 0 || l[f] >= n || u[f] < 0 || u[f] >= n || l[f] == u[f]) { free(ord); return -1; }
+        ord[f] = f;
+    }
+    g_sort_l = l; g_sort_u = u;
+    qsort(ord, (size_t)nf, sizeof(int), cmp_face);
+    D->l = malloc(sizeof(int) * (size_t)(nf + 1));
+    D->u = malloc(sizeof(int) * (size_t)(nf + 1));
+    D->a = malloc(sizeof(double) * (size_t)(nf + 1));
+    D->rD = malloc(sizeof(double) * (size_t)n);
+    int m = 0;
+    for (int k = 0; k < nf; ++k) {
+        int f = ord[k];
+        int lo = l[f] < u[f] ? l[f] : u[f], hi = l[f] < u[f] ? u[f] : l[f];
+        if (nb > 1 && block_of(nb, start, lo) != block_of(nb, start, hi)) continue;
+        if (m > 0 && D->l[m - 1] == lo && D->u[m - 1] == hi) { D->a[m - 1] += upper[f]; continue; }
+        D->l[m] = lo; D->u[m] = hi; D->a[m] = upper[f]; ++m;
+    }
+    D->nf = m;
+    free(ord);
+    for (int c = 0; c < n; ++c) D->rD[c] = diag[c];                   /* calcReciprocalD */
+    for (int f = 0; f < m; ++f) D->rD[D->u[f]] -= D->a[f] * D->a[f] / D->rD[D->l[f]];
+    for (int c = 0; c < n; ++c) {
+        if (!(D->rD[c] > 0.0) || !isfinite(D->rD[c])) return -2;
+        D->rD[c] = 1.0 / D->rD[c];
+    }
+    return 0;
+}
+
+static void dic_free(dic_t *D) { free(D->l); free(D->u); free(D->a); free(D->rD); }
+
+typedef struct { int n; dic_t D; } dic_ctx_t;
+
+static void dic_precondition(const void *ctx, const double *r, double *w)
+{
+    const dic_ctx_t *C = (const dic_ctx_t *)ctx;
+    const dic_t *D = &C->D;
+    for (int c = 0; c < C->n; ++c) w[c] = D->rD[c] * r[c];
+    for (int f = 0; f < D->nf; ++f) w[D->u[f]] -= D->rD[D->u[f]] * D->a[f] * w[D->l[f]];
+    for (int f = D->nf - 1; f >= 0; --f) w[D->l[f]] -= D->rD[D->l[f]] * D->a[f] * w[D->u[f]];
+}
+
+/* rD out [n] (the reciprocal D) and, if r != NULL, w = M^-1 r.  nb = 1: whole matrix. */
+int oracle_dic(int n, int nf, const int *l, const int *u, const double *diag,
+               const double *upper, int nb, const int *start, double *rD, const double *r,
+               double *w)
+{
+    dic_ctx_t C = {n, {0}};
+    int st = dic_make(n, nf, l, u, diag, upper, nb, start, &C.D);
+    if (st == -1) return OR_ERR_ARG;
+    if (st == -2) { dic_free(&C.D); return OR_BREAKDOWN; }
+    if (rD) memcpy(rD, C.D.rD, sizeof(double) * (size_t)n);
+    if (r && w) dic_precondition(&C, r, w);
+    dic_free(&C.D);
+    return OR_OK;
+}
+
+/* DIC-preconditioned CG (c2 with z = M^-1 r) and pipelined CG (c3 literal form, u = M^-1 r,
+ * m = M^-1 w); same criteria and stopping rules as the Jacobi solvers above. */
+int oracle_dic_pcg(int n, int nf, const int *l, const int *u, const double *diag,
+                   const double *upper, const double *b, double *x, double tol, int maxIter,
+                   int norm, int *nIter, double *finalRes, double *hist, double relTol,
+                   int minIter, int nb, const int *start, int pipelined)
+{
+    dic_ctx_t C = {n, {0}};
+    int st = dic_make(n, nf, l, u, diag, upper, nb, start, &C.D);
+    if (st == -1) return OR_ERR_ARG;
+    if (st == -2) { dic_free(&C.D); return OR_BREAKDOWN; }
+    prec_t M = {dic_precondition, &C};
+    st = pipelined ? pipecg_core(n, nf, l, u, diag, NULL, upper, b, x, tol, maxIter, norm, 0,
+                                 nIter, finalRes, hist, relTol, minIter, &M, 0)
+                   : pcg_core(n, nf, l, u, diag, NULL, upper, b, x, tol, maxIter, norm, nIter,
+                              finalRes, hist, relTol, minIter, &M);
+    dic_free(&C.D);
+    return st;
+}
