@@ -265,6 +265,40 @@ ldu_status amg_pcg_solve(ldu_handle h, const double *b, double *x, double tol, i
 ldu_status amg_pipecg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,
                             const ldu_solve_opts *opts, int *nIter, double *finalRes);
 
+/* ---- DIC preconditioner ------------------------------------------------
+ * OpenFOAM's default preconditioner for the pressure solve (DICPreconditioner [ext]; NEXT-1 "Optional
+ * DIC preconditioner (OpenFOAM's default for p)"), readings Z35-Z36:
+ *   M = (D + L) D^-1 (D + L^T), L = strictly-lower part of the local matrix,
+ *   D_c = A_cc - sum_{l < c} A_cl^2 / D_l  (so diag(M) = diag(A); IC(0) on hex meshes);
+ *   z = M^-1 r by a forward and a backward triangular sweep.
+ * The sweeps are level-scheduled on the device (a cell's level = 1 + the largest level of its
+ * lower neighbours; one launch per level and sweep: 3n-2 levels on an n^3 lexicographic hex mesh),
+ * so results equal the sequential face loops up to the summation order within a row.  Multi-rank
+ * handles: the factor of the rank's local matrix (interfaces dropped), i.e. block-Jacobi DIC, as
+ * OpenFOAM does on processor boundaries; ldu_dic_setup is then local, the solves collective.
+ * Symmetric matrices only.  A setup replaces any AMG hierarchy on the handle and vice versa.
+ * Errors: INVALID_ARG (non-symmetric matrix), STATE (a pivot D_c <= 0; or, for the calls below,
+ * no DIC factor), CUDA, OOM. */
+typedef struct {
+  int nLevels;              /* number of level-scheduling levels                                  */
+  int widestLevel;          /* cells in the widest level                                          */
+  long long lowerEntries;   /* stored strictly-lower couplings (non-zero)                         */
+  double setupMs;           /* device + host time of ldu_dic_setup                                */
+} ldu_dic_info;
+
+ldu_status ldu_dic_setup(ldu_handle h);
+/* rD: [nCells] host or device or NULL, receives 1 / D_c; info may be NULL. */
+ldu_status ldu_dic_get(ldu_handle h, double *rD, ldu_dic_info *info);
+/* z = M^-1 r.  r, z: [nCells] host or device, must not alias. */
+ldu_status ldu_dic_apply(ldu_handle h, const double *r, double *z);
+/* DIC-preconditioned classical CG (c2 with z = M^-1 r) and pipelined CG (c3 literal GV form with
+ * u = M^-1 r, m = M^-1 w; one fused reduction per iteration).  Same arguments, options and
+ * semantics as amg_pcg_solve / amg_pipecg_solve (replaceEvery unsupported). */
+ldu_status dic_pcg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,
+                         const ldu_solve_opts *opts, int *nIter, double *finalRes);
+ldu_status dic_pipecg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,
+                            const ldu_solve_opts *opts, int *nIter, double *finalRes);
+
 ldu_status ldu_destroy(ldu_handle h);
 const char *ldu_last_error(void);
 int ldu_abi_version(void);

@@ -112,6 +112,15 @@ class AmgInfo(ctypes.Structure):
                 "setupMs": self.setupMs, "deviceBytes": self.deviceBytes}
 
 
+class DicInfo(ctypes.Structure):
+    """ldu_dic_info (include/ldu.h)."""
+    _fields_ = [("nLevels", ctypes.c_int), ("widestLevel", ctypes.c_int),
+                ("lowerEntries", ctypes.c_longlong), ("setupMs", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _D = ctypes.c_double
@@ -145,6 +154,13 @@ SIGNATURES = {
     "amg_pcg_solve": (_S, [_P, _P, _P, _D, _I, ctypes.POINTER(SolveOpts), ctypes.POINTER(_I),
                            ctypes.POINTER(_D)]),
     "amg_pipecg_solve": (_S, [_P, _P, _P, _D, _I, ctypes.POINTER(SolveOpts), ctypes.POINTER(_I),
+                              ctypes.POINTER(_D)]),
+    "ldu_dic_setup": (_S, [_P]),
+    "ldu_dic_get": (_S, [_P, _P, ctypes.POINTER(DicInfo)]),
+    "ldu_dic_apply": (_S, [_P, _P, _P]),
+    "dic_pcg_solve": (_S, [_P, _P, _P, _D, _I, ctypes.POINTER(SolveOpts), ctypes.POINTER(_I),
+                           ctypes.POINTER(_D)]),
+    "dic_pipecg_solve": (_S, [_P, _P, _P, _D, _I, ctypes.POINTER(SolveOpts), ctypes.POINTER(_I),
                               ctypes.POINTER(_D)]),
     "ldu_destroy": (_S, [_P]),
 }
@@ -334,6 +350,41 @@ class LduMatrix:
                          profile: bool = False, relTol: float = 0.0, minIter: int = 0):
         """AMG-preconditioned pipelined CG (literal GV form); x is in/out."""
         return self._solve(_lib.amg_pipecg_solve, b, x, tol, maxIter, norm, record_history,
+                           batch, profile, relTol, minIter)
+
+    # -- DIC preconditioner (NEXT-1; OpenFOAM's default for p) --------------------------------
+    def dic_setup(self) -> dict:
+        """Level analysis + factor on the device; returns dic_info()."""
+        _check(_lib.ldu_dic_setup(self.handle))
+        return self.dic_info()
+
+    def dic_info(self) -> dict:
+        i = DicInfo()
+        _check(_lib.ldu_dic_get(self.handle, None, ctypes.byref(i)))
+        return i.as_dict()
+
+    def dic_rD(self, out):
+        """out[c] = 1 / D_c of the factor (host or device array)."""
+        _check(_lib.ldu_dic_get(self.handle, _ptr(out, "f64"), None))
+        return out
+
+    def dic_apply(self, r, z):
+        """z = M^-1 r (forward + backward level-scheduled sweeps)."""
+        _check(_lib.ldu_dic_apply(self.handle, _ptr(r, "f64"), _ptr(z, "f64")))
+        return z
+
+    def dic_pcg_solve(self, b, x, tol: float = 1e-10, maxIter: int = 10000, norm: int = NORM_L2,
+                      record_history: bool = False, batch: int = 0, profile: bool = False,
+                      relTol: float = 0.0, minIter: int = 0):
+        """DIC-preconditioned CG; x is in/out.  Returns (status, nIter, finalRes)."""
+        return self._solve(_lib.dic_pcg_solve, b, x, tol, maxIter, norm, record_history, batch,
+                           profile, relTol, minIter)
+
+    def dic_pipecg_solve(self, b, x, tol: float = 1e-10, maxIter: int = 10000,
+                         norm: int = NORM_L2, record_history: bool = False, batch: int = 0,
+                         profile: bool = False, relTol: float = 0.0, minIter: int = 0):
+        """DIC-preconditioned pipelined CG (literal GV form); x is in/out."""
+        return self._solve(_lib.dic_pipecg_solve, b, x, tol, maxIter, norm, record_history,
                            batch, profile, relTol, minIter)
 
     def history(self):

@@ -81,7 +81,33 @@ struct AmgLevel {
   bool ownsDiag = false;
 };
 
+enum { PREC_AMG = 0, PREC_DIC = 1 };
+
+// DIC factor (reading Z35): cells in level order (a cell's level = 1 + the
+// largest level of its lower neighbours, so every cell of a level depends only on earlier levels
+// in the forward sweep and on later levels in the backward sweep), with each cell's strictly-lower
+// and strictly-upper couplings stored row by row in that order.
+struct DicFactor {
+  int nLev = 0;
+  std::vector<int> levPtr;       // host [nLev + 1] positions in perm
+  int* perm = nullptr;           // [n] cell at level-order position k
+  int *loPtr = nullptr, *loCol = nullptr;   // [n + 1], [nnzL]
+  double* loVal = nullptr;
+  int *upPtr = nullptr, *upCol = nullptr;   // [n + 1], [nnzU]
+  double* upVal = nullptr;
+  double* rD = nullptr;          // [n] reciprocal D of M = (D + L) D^-1 (D + L^T), by cell
+  // level order is padded so that each level starts on a warp boundary (perm = -1 in the gaps):
+  // no warp ever holds two levels, so the sync-free sweeps never wait inside a warp
+  int nPad = 0;                  // padded positions
+  unsigned* flag = nullptr;      // [n] per-cell epoch tag of the sync-free sweeps
+  unsigned* ctl = nullptr;       // [3] epoch, forward ticket, backward ticket
+  long long nnzL = 0;
+  int maxLevel = 0;              // cells in the widest level
+};
+
 struct AmgHierarchy {
+  int kind = PREC_AMG;       // PREC_AMG: the hierarchy below; PREC_DIC: `dic` (L = 0, no levels)
+  DicFactor dic;
   ldu_amg_opts opts{};
   std::vector<AmgLevel> lv;  // levels 0 .. L-1
   int L = 0;
@@ -102,13 +128,15 @@ struct AmgHierarchy {
 };
 
 void amg_setup(ldu_handle h, const ldu_amg_opts* opts);
+void dic_setup(ldu_handle h);
+void dic_export(ldu_handle h, double* rD, ldu_dic_info* info);
 void amg_release(ldu_handle h);
 void amg_info(ldu_handle h, ldu_amg_info* out);
 void amg_export(ldu_handle h, int level, int which, int* ptr, int* col, double* val);
 void amg_export_agg(ldu_handle h, int level, int* agg);
 // ldu_solve.cu
-void amg_vcycle(ldu_handle h, const double* r, double* z);
-ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, double tol,
+void amg_vcycle(ldu_handle h, const double* r, double* z, int kind);
+ldu_status amg_solve(ldu_handle h, int kind, bool pipelined, const double* b, double* x, double tol,
                      int maxIter, const ldu_solve_opts* opts, int* nIter, double* finalRes);
 
 // Priority key of node i in the MIS-2 rounds (reading Z30): keyMode 0 = index, 1 = the

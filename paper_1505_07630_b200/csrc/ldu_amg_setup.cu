@@ -1131,6 +1131,10 @@ void amg_release(ldu_handle h) {
     if (g) cudaGraphExecDestroy(g);
   for (AmgLevel& L : H->lv) free_level(L);
   H->Ac.release();
+  DicFactor& D = H->dic;
+  for (void* p : {(void*)D.perm, (void*)D.loPtr, (void*)D.loCol, (void*)D.loVal, (void*)D.upPtr,
+                  (void*)D.upCol, (void*)D.upVal, (void*)D.rD, (void*)D.flag, (void*)D.ctl})
+    dfree(p);
   for (void* p : {(void*)H->Ainv, (void*)H->fL, (void*)H->zL, (void*)H->u, (void*)H->m,
                   (void*)H->zk, (void*)H->qk})
     dfree(p);
@@ -1265,7 +1269,7 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
 
 void amg_info(ldu_handle h, ldu_amg_info* out) {
   AmgHierarchy* H = h->amg;
-  if (!H) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+  if (!H || H->kind != PREC_AMG) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
   std::memset(out, 0, sizeof(*out));
   out->nLevels = H->L;
   out->coarsestN = H->nc;
@@ -1292,7 +1296,7 @@ void amg_info(ldu_handle h, ldu_amg_info* out) {
 
 void amg_export(ldu_handle h, int level, int which, int* ptr, int* col, double* val) {
   AmgHierarchy* H = h->amg;
-  if (!H) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+  if (!H || H->kind != PREC_AMG) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
   if (which < 0 || which > 2) fail_arg("which must be 0 (A), 1 (P) or 2 (R)");
   const int maxLevel = which == 0 ? H->L : H->L - 1;
   if (level < 0 || level > maxLevel) fail_arg("level out of range");
@@ -1305,10 +1309,174 @@ void amg_export(ldu_handle h, int level, int which, int* ptr, int* col, double* 
 
 void amg_export_agg(ldu_handle h, int level, int* agg) {
   AmgHierarchy* H = h->amg;
-  if (!H) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+  if (!H || H->kind != PREC_AMG) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
   if (level < 0 || level >= H->L) fail_arg("level out of range");
   if (!agg) fail_arg("agg is NULL");
   CUDA_CHECK(cudaMemcpy(agg, H->lv[level].agg, sizeof(int) * H->lv[level].n, cudaMemcpyDefault));
+}
+
+// ---------------------------------------------------------------------------------------------
+// DIC preconditioner (readings Z35, Z36)
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+// D_c = diag_c - sum_{lower l} a_cl^2 / D_l over one level (all lower neighbours are final)
+__global__ void k_dic_rD(int beg, int end, const int* __restrict__ perm,
+                         const int* __restrict__ ptr, const int* __restrict__ col,
+                         const double* __restrict__ val, const double* __restrict__ diag,
+                         double* rD, int* bad) {
+  for (int k = beg + blockIdx.x * blockDim.x + threadIdx.x; k < end; k += gridDim.x * blockDim.x) {
+    const int c = perm[k];
+    if (c < 0) continue;
+    double d = diag[c];
+    for (int j = ptr[k]; j < ptr[k + 1]; ++j) {
+      const double a = val[j];
+      d -= a * a * rD[col[j]];
+    }
+    if (!(d > 0.0) || !isfinite(d)) *bad = 1;
+    rD[c] = 1.0 / d;
+  }
+}
+
+}  // namespace
+
+// The level analysis runs once on the host (a single pass in cell order: every lower neighbour
+// of a cell has a smaller index); the factor itself (D) is computed on the device level by level.
+void dic_setup(ldu_handle h) {
+  if (!h->symmetric) fail_arg("DIC requires a symmetric matrix (lower == NULL or lower == upper)");
+  amg_release(h);
+  cudaStream_t s = h->own_stream;
+  if (h->stream != h->own_stream) {
+    CUDA_CHECK(cudaEventRecord(h->ev_fork, h->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_fork, 0));
+  }
+  CUDA_CHECK(cudaEventRecord(h->ev[0], s));
+  AmgHierarchy* H = new AmgHierarchy();
+  H->kind = PREC_DIC;
+  h->amg = H;
+  try {
+    const int n = h->n;
+    CsrMat A = level0_csr(h, s);  // local rows: interfaces dropped (block-Jacobi, Z33 / Z35)
+    std::vector<int> ptr(n + 1), col(A.nnz);
+    std::vector<double> val(A.nnz);
+    CUDA_CHECK(cudaMemcpyAsync(ptr.data(), A.ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(col.data(), A.col, sizeof(int) * A.nnz, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(val.data(), A.val, sizeof(double) * A.nnz, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    A.release();
+    // levels (a zero coefficient is not a dependency, Z36)
+    std::vector<int> lev(n, 0);
+    int nLev = 0;
+    long long nnzL = 0, nnzU = 0;
+    for (int r = 0; r < n; ++r) {
+      int lv = 0;
+      for (int j = ptr[r]; j < ptr[r + 1]; ++j)
+        if (val[j] != 0.0) {
+          if (col[j] < r) {
+            lv = std::max(lv, lev[col[j]] + 1);
+            ++nnzL;
+          } else if (col[j] > r) {
+            ++nnzU;
+          }
+        }
+      lev[r] = lv;
+      nLev = std::max(nLev, lv + 1);
+    }
+    DicFactor& D = H->dic;
+    D.nLev = nLev;
+    D.nnzL = nnzL;
+    std::vector<int> cnt(nLev, 0);
+    for (int r = 0; r < n; ++r) cnt[lev[r]]++;
+    D.levPtr.assign(nLev + 1, 0);
+    for (int l = 0; l < nLev; ++l) {
+      D.maxLevel = std::max(D.maxLevel, cnt[l]);
+      D.levPtr[l + 1] = D.levPtr[l] + (cnt[l] + 31) / 32 * 32;  // warp-aligned levels
+    }
+    const int nPad = D.levPtr[nLev];
+    D.nPad = nPad;
+    std::vector<int> perm(nPad, -1), pos(D.levPtr.begin(), D.levPtr.end() - 1);
+    for (int r = 0; r < n; ++r) perm[pos[lev[r]]++] = r;  // ascending cell index within a level
+    std::vector<int> lp(nPad + 1), lc(nnzL), up(nPad + 1), uc(nnzU);
+    std::vector<double> lvv(nnzL), uvv(nnzU);
+    long long ol = 0, ou = 0;
+    for (int k = 0; k < nPad; ++k) {
+      const int r = perm[k];
+      lp[k] = (int)ol;
+      up[k] = (int)ou;
+      if (r < 0) continue;
+      for (int j = ptr[r]; j < ptr[r + 1]; ++j) {
+        if (val[j] == 0.0) continue;
+        if (col[j] < r) {
+          lc[ol] = col[j];
+          lvv[ol++] = val[j];
+        } else if (col[j] > r) {
+          uc[ou] = col[j];
+          uvv[ou++] = val[j];
+        }
+      }
+    }
+    lp[nPad] = (int)ol;
+    up[nPad] = (int)ou;
+    D.perm = dmalloc<int>(nPad);
+    D.loPtr = dmalloc<int>(nPad + 1);
+    D.loCol = dmalloc<int>(std::max(1LL, nnzL));
+    D.loVal = dmalloc<double>(std::max(1LL, nnzL));
+    D.upPtr = dmalloc<int>(nPad + 1);
+    D.upCol = dmalloc<int>(std::max(1LL, nnzU));
+    D.upVal = dmalloc<double>(std::max(1LL, nnzU));
+    D.rD = dmalloc<double>(n);
+    D.flag = dmalloc<unsigned>(n);
+    D.ctl = dmalloc<unsigned>(3);
+    CUDA_CHECK(cudaMemsetAsync(D.flag, 0, sizeof(unsigned) * n, s));
+    {
+      static const unsigned ctl0[3] = {1u, 0u, 0u};
+      CUDA_CHECK(cudaMemcpyAsync(D.ctl, ctl0, sizeof(ctl0), cudaMemcpyHostToDevice, s));
+    }
+    auto up_h2d = [&](void* d, const void* hsrc, size_t bytes) {
+      if (bytes) CUDA_CHECK(cudaMemcpyAsync(d, hsrc, bytes, cudaMemcpyHostToDevice, s));
+    };
+    up_h2d(D.perm, perm.data(), sizeof(int) * nPad);
+    up_h2d(D.loPtr, lp.data(), sizeof(int) * (nPad + 1));
+    up_h2d(D.loCol, lc.data(), sizeof(int) * nnzL);
+    up_h2d(D.loVal, lvv.data(), sizeof(double) * nnzL);
+    up_h2d(D.upPtr, up.data(), sizeof(int) * (nPad + 1));
+    up_h2d(D.upCol, uc.data(), sizeof(int) * nnzU);
+    up_h2d(D.upVal, uvv.data(), sizeof(double) * nnzU);
+    {
+      Scratch sc(s);
+      int* bad = sc.get<int>(1);
+      CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+      for (int l = 0; l < nLev; ++l) {
+        const int b = D.levPtr[l], e = D.levPtr[l + 1];
+        k_dic_rD<<<nblk(e - b), kSB, 0, s>>>(b, e, D.perm, D.loPtr, D.loCol, D.loVal, h->diag,
+                                             D.rD, bad);
+      }
+      CUDA_CHECK(cudaGetLastError());
+      if (d2h(bad, s)) throw Error(LDU_ERR_STATE, "DIC: non-positive pivot");
+    }
+    CUDA_CHECK(cudaEventRecord(h->ev[1], s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+    H->setupMs = ms;
+  } catch (...) {
+    cudaStreamSynchronize(s);
+    amg_release(h);
+    throw;
+  }
+}
+
+void dic_export(ldu_handle h, double* rD, ldu_dic_info* info) {
+  AmgHierarchy* H = h->amg;
+  if (!H || H->kind != PREC_DIC) throw Error(LDU_ERR_STATE, "no DIC factor (call ldu_dic_setup)");
+  if (rD) CUDA_CHECK(cudaMemcpy(rD, H->dic.rD, sizeof(double) * h->n, cudaMemcpyDefault));
+  if (info) {
+    std::memset(info, 0, sizeof(*info));
+    info->nLevels = H->dic.nLev;
+    info->widestLevel = H->dic.maxLevel;
+    info->lowerEntries = H->dic.nnzL;
+    info->setupMs = H->setupMs;
+  }
 }
 
 }  // namespace ldu

@@ -404,12 +404,158 @@ void amg_grids(ldu_handle h) {
     throw Error(LDU_ERR_STATE, "AMG grid exceeds the reduction slots");
 }
 
+// ---- DIC preconditioner (NEXT-1, reading Z35): level-scheduled triangular sweeps --------------
+// forward:  z_c = rD_c (f_c - sum_{lower j} a_cj z_j)      levels ascending
+// backward: z_c -= rD_c sum_{upper j} a_cj z_j              levels descending
+// One thread per cell of the level; the level's cells read only z of earlier launches.
+__global__ void __launch_bounds__(kBlock) k_dic_fwd(int beg, int end, const int* __restrict__ perm,
+                                                    const int* __restrict__ ptr,
+                                                    const int* __restrict__ col,
+                                                    const double* __restrict__ val,
+                                                    const double* __restrict__ rD,
+                                                    const double* __restrict__ f, double* z,
+                                                    const State* st) {
+  if (st && st->done) return;
+  for (int k = beg + blockIdx.x * blockDim.x + threadIdx.x; k < end; k += gridDim.x * blockDim.x) {
+    const int c = __ldg(perm + k);
+    if (c < 0) continue;
+    double s = __ldg(f + c);
+    const int j1 = __ldg(ptr + k + 1);
+    for (int j = __ldg(ptr + k); j < j1; ++j) s = fma(-__ldg(val + j), z[__ldg(col + j)], s);
+    z[c] = __ldg(rD + c) * s;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_dic_bwd(int beg, int end, const int* __restrict__ perm,
+                                                    const int* __restrict__ ptr,
+                                                    const int* __restrict__ col,
+                                                    const double* __restrict__ val,
+                                                    const double* __restrict__ rD, double* z,
+                                                    const State* st) {
+  if (st && st->done) return;
+  for (int k = beg + blockIdx.x * blockDim.x + threadIdx.x; k < end; k += gridDim.x * blockDim.x) {
+    const int c = __ldg(perm + k);
+    if (c < 0) continue;
+    double s = 0.0;
+    const int j1 = __ldg(ptr + k + 1);
+    for (int j = __ldg(ptr + k); j < j1; ++j) s = fma(__ldg(val + j), z[__ldg(col + j)], s);
+    if (j1 > __ldg(ptr + k)) z[c] = fma(-__ldg(rD + c), s, z[c]);
+  }
+}
+
+// Sync-free variant (opt-in, LDU_DIC_SF): ONE persistent launch per sweep.  Blocks take 256-position chunks
+// of the (warp-aligned) level order from a ticket counter, so a chunk only ever waits for chunks
+// taken earlier by running blocks (no deadlock, any grid size), and no warp waits on itself
+// (levels start on warp boundaries).  A cell spins until each neighbour it reads carries this
+// sweep's epoch tag (fence + volatile tag store after its z store; volatile polls with
+// __nanosleep back-off, then a fence before the reads), i.e. the
+// dependency is per cell, not per level: the critical path is one flag hand-off per level.
+
+template <bool FWD, int SLEEP_NS>
+__global__ void __launch_bounds__(kBlock) k_dic_sweep_sf(int nPad, const int* __restrict__ perm,
+                                                         const int* __restrict__ ptr,
+                                                         const int* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ rD,
+                                                         const double* __restrict__ f, double* z,
+                                                         unsigned* flag, unsigned* ctl,
+                                                         const State* st) {
+  if (st && st->done) return;
+  __shared__ int chunk;
+  const unsigned tag = 2u * ctl[0] + (FWD ? 1u : 2u);
+  unsigned* ticket = ctl + (FWD ? 1 : 2);
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) chunk = (int)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const long long base = (long long)chunk * kBlock;
+    if (base >= nPad) return;
+    const long long q = base + threadIdx.x;
+    if (q >= nPad) continue;
+    const int k = FWD ? (int)q : nPad - 1 - (int)q;
+    const int c = __ldg(perm + k);
+    if (c < 0) continue;
+    const int j0 = __ldg(ptr + k), j1 = __ldg(ptr + k + 1);
+    double s = FWD ? __ldg(f + c) : 0.0;
+    // wait (relaxed polls with back-off) for every neighbour, then one acquire fence
+    for (int j = j0; j < j1; ++j) {
+      const volatile unsigned* fl = flag + __ldg(col + j);
+      while (*fl != tag) __nanosleep(SLEEP_NS);
+    }
+    __threadfence();
+    for (int j = j0; j < j1; ++j) {
+      const double v = __ldg(val + j) * __ldcg(z + __ldg(col + j));
+      s = FWD ? s - v : s + v;
+    }
+    if (FWD) {
+      z[c] = __ldg(rD + c) * s;
+    } else if (j1 > j0) {
+      z[c] = fma(-__ldg(rD + c), s, __ldcg(z + c));
+    }
+    __threadfence();
+    *(volatile unsigned*)(flag + c) = tag;
+  }
+}
+
+// next epoch, tickets back to 0 (stream-ordered after both sweeps)
+__global__ void k_dic_bump(unsigned* ctl, const State* st) {
+  if (st && st->done) return;
+  ctl[0] += 1u;
+  ctl[1] = 0u;
+  ctl[2] = 0u;
+}
+
+long long enqueue_dic(ldu_handle h, const double* f0, double* z0, cudaStream_t s, State* st,
+                      const Red* rho) {
+  const DicFactor& D = h->amg->dic;
+  auto grid = [](int m) { return (int)std::max(1, std::min((m + kBlock - 1) / kBlock, 148 * 8)); };
+  long long kernels = 0;
+  // LDU_DIC_SF = back-off in ns of the sync-free sweeps (0 = one launch per level, the default)
+  static const int sf = std::getenv("LDU_DIC_SF") ? std::atoi(std::getenv("LDU_DIC_SF")) : 0;
+  static const int sfBlocks = std::getenv("LDU_DIC_SF_BLOCKS") ? std::atoi(std::getenv("LDU_DIC_SF_BLOCKS")) : 148 * 4;
+  if (!sf) {  // one launch per level and sweep (measured reference variant)
+    for (int l = 0; l < D.nLev; ++l) {
+      const int b = D.levPtr[l], e = D.levPtr[l + 1];
+      k_dic_fwd<<<grid(e - b), kBlock, 0, s>>>(b, e, D.perm, D.loPtr, D.loCol, D.loVal, D.rD, f0,
+                                               z0, st);
+    }
+    // the last level has no upper neighbours: the backward sweep starts one level down
+    for (int l = D.nLev - 2; l >= 0; --l) {
+      const int b = D.levPtr[l], e = D.levPtr[l + 1];
+      k_dic_bwd<<<grid(e - b), kBlock, 0, s>>>(b, e, D.perm, D.upPtr, D.upCol, D.upVal, D.rD, z0,
+                                               st);
+    }
+    kernels += D.nLev + std::max(0, D.nLev - 1);
+  } else {
+    // the backward sweep's first cell (highest level) sets its tag without waiting; every
+    // upper neighbour it reads was tagged earlier in the same sweep
+    const int g = std::max(1, std::min(sfBlocks, (D.nPad + kBlock - 1) / kBlock));
+    auto sweeps = [&](auto fwd, auto bwd) {
+      fwd<<<g, kBlock, 0, s>>>(D.nPad, D.perm, D.loPtr, D.loCol, D.loVal, D.rD, f0, z0, D.flag,
+                               D.ctl, st);
+      bwd<<<g, kBlock, 0, s>>>(D.nPad, D.perm, D.upPtr, D.upCol, D.upVal, D.rD, f0, z0, D.flag,
+                               D.ctl, st);
+    };
+    if (sf >= 256) sweeps(k_dic_sweep_sf<true, 256>, k_dic_sweep_sf<false, 256>);
+    else if (sf >= 64) sweeps(k_dic_sweep_sf<true, 64>, k_dic_sweep_sf<false, 64>);
+    else sweeps(k_dic_sweep_sf<true, 16>, k_dic_sweep_sf<false, 16>);
+    k_dic_bump<<<1, 1, 0, s>>>(D.ctl, st);
+    kernels += 3;
+  }
+  if (rho) {
+    k_amg_dot<<<h->grid, kBlock, 0, s>>>(h->n, z0, f0, st, *rho);
+    ++kernels;
+  }
+  return kernels;
+}
+
 // ---- V-cycle enqueue --------------------------------------------------------------------------
 // z0 = B f0 on stream s.  st != nullptr: every kernel exits at entry once the solve is done.
 // rho != nullptr: level-0 post-sweep (or the direct solve) also reduces (z0, f0) into rho's control.
 long long enqueue_vcycle(ldu_handle h, const double* f0, double* z0, cudaStream_t s, State* st,
                          const Red* rho) {
   AmgHierarchy* H = h->amg;
+  if (H->kind == PREC_DIC) return enqueue_dic(h, f0, z0, s, st, rho);
   long long kernels = 0;
   const int L = H->L;
   for (int l = 0; l < L; ++l) {
@@ -571,8 +717,14 @@ long long enqueue_amg_iters(ldu_handle h, bool pipelined, int batch, cudaStream_
 // ---------------------------------------------------------------------------------------------
 // public-internal entry points
 // ---------------------------------------------------------------------------------------------
-void amg_vcycle(ldu_handle h, const double* r, double* z) {
-  if (!h->amg) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
+static void check_prec(ldu_handle h, int kind) {
+  if (!h->amg || h->amg->kind != kind)
+    throw Error(LDU_ERR_STATE, kind == PREC_DIC ? "no DIC factor (call ldu_dic_setup)"
+                                                : "no AMG hierarchy (call ldu_amg_setup)");
+}
+
+void amg_vcycle(ldu_handle h, const double* r, double* z, int kind) {
+  check_prec(h, kind);
   amg_grids(h);
   if (!r || !z) fail_arg("r and z must not be NULL");
   cudaStream_t s = h->own_stream;
@@ -614,17 +766,18 @@ void amg_vcycle(ldu_handle h, const double* r, double* z) {
   h->stats.iterMs = ms;
 }
 
-ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, double tol,
-                     int maxIter, const ldu_solve_opts* opts, int* nIter, double* finalRes) {
+ldu_status amg_solve(ldu_handle h, int kind, bool pipelined, const double* b, double* x,
+                     double tol, int maxIter, const ldu_solve_opts* opts, int* nIter,
+                     double* finalRes) {
+  check_prec(h, kind);
   AmgHierarchy* H = h->amg;
-  if (!H) throw Error(LDU_ERR_STATE, "no AMG hierarchy (call ldu_amg_setup)");
   if (!b || !x) fail_arg("b and x must not be NULL");
   if (!(tol >= 0.0)) fail_arg("tol must be >= 0");
   if (maxIter < 0) fail_arg("maxIter must be >= 0");
   ldu_solve_opts o{};
   if (opts) {
     o = *opts;
-    if (o.replaceEvery) fail_arg("replaceEvery is not supported by the AMG solvers");
+    if (o.replaceEvery) fail_arg("replaceEvery is not supported by the AMG / DIC solvers");
     if (o.reserved2[0] != 0.0 || o.reserved2[1] != 0.0)
       fail_arg("ldu_solve_opts.reserved2 must be zero");
   }
@@ -634,7 +787,7 @@ ldu_status amg_solve(ldu_handle h, bool pipelined, const double* b, double* x, d
   if (o.batch < 0) fail_arg("batch must be >= 0");
   if (o.profile != 0 && o.profile != 1) fail_arg("profile must be 0 or 1");
   const bool profile = o.profile == 1;
-  const int batch = o.batch ? o.batch : 8;
+  const int batch = o.batch ? o.batch : (kind == PREC_DIC ? 2 : 8);  // DIC: ~2 nLev nodes/iter
 
   ensure_amg_work(h, pipelined);
   amg_grids(h);

@@ -306,7 +306,7 @@ ldu_status ldu_amg_vcycle(ldu_handle h, const double* r, double* z) {
   return guard("ldu_amg_vcycle", [&] {
     if (!h) ldu::fail_arg("handle is NULL");
     CUDA_CHECK(cudaSetDevice(h->device));
-    ldu::amg_vcycle(h, r, z);
+    ldu::amg_vcycle(h, r, z, ldu::PREC_AMG);
     return LDU_OK;
   });
 }
@@ -316,7 +316,7 @@ ldu_status amg_pcg_solve(ldu_handle h, const double* b, double* x, double tol, i
   return guard("amg_pcg_solve", [&] {
     if (!h) ldu::fail_arg("handle is NULL");
     CUDA_CHECK(cudaSetDevice(h->device));
-    return ldu::amg_solve(h, false, b, x, tol, maxIter, opts, nIter, finalRes);
+    return ldu::amg_solve(h, ldu::PREC_AMG, false, b, x, tol, maxIter, opts, nIter, finalRes);
   });
 }
 
@@ -325,7 +325,52 @@ ldu_status amg_pipecg_solve(ldu_handle h, const double* b, double* x, double tol
   return guard("amg_pipecg_solve", [&] {
     if (!h) ldu::fail_arg("handle is NULL");
     CUDA_CHECK(cudaSetDevice(h->device));
-    return ldu::amg_solve(h, true, b, x, tol, maxIter, opts, nIter, finalRes);
+    return ldu::amg_solve(h, ldu::PREC_AMG, true, b, x, tol, maxIter, opts, nIter, finalRes);
+  });
+}
+
+ldu_status ldu_dic_setup(ldu_handle h) {
+  return guard("ldu_dic_setup", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    ldu::dic_setup(h);
+    return LDU_OK;
+  });
+}
+
+ldu_status ldu_dic_get(ldu_handle h, double* rD, ldu_dic_info* info) {
+  return guard("ldu_dic_get", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    ldu::dic_export(h, rD, info);
+    return LDU_OK;
+  });
+}
+
+ldu_status ldu_dic_apply(ldu_handle h, const double* r, double* z) {
+  return guard("ldu_dic_apply", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    ldu::amg_vcycle(h, r, z, ldu::PREC_DIC);
+    return LDU_OK;
+  });
+}
+
+ldu_status dic_pcg_solve(ldu_handle h, const double* b, double* x, double tol, int maxIter,
+                         const ldu_solve_opts* opts, int* nIter, double* finalRes) {
+  return guard("dic_pcg_solve", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    return ldu::amg_solve(h, ldu::PREC_DIC, false, b, x, tol, maxIter, opts, nIter, finalRes);
+  });
+}
+
+ldu_status dic_pipecg_solve(ldu_handle h, const double* b, double* x, double tol, int maxIter,
+                            const ldu_solve_opts* opts, int* nIter, double* finalRes) {
+  return guard("dic_pipecg_solve", [&] {
+    if (!h) ldu::fail_arg("handle is NULL");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    return ldu::amg_solve(h, ldu::PREC_DIC, true, b, x, tol, maxIter, opts, nIter, finalRes);
   });
 }
 

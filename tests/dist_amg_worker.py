@@ -6,6 +6,8 @@ the halo exchange in the Krylov SpMV.  Rank 0 compares with the oracle's serial 
 (oracle.amg.block_hierarchies + amg_block_solve on the global system): per-rank hierarchy sizes
 and level-0 aggregates bit-exact, iteration counts within +-2 % (+-1), solution rel-L2 <= 1e-8 at
 tol 1e-10, fixed-iteration residual histories.  Prints "DIST_AMG_OK <json>" on success.
+With argument "dic" the same checks run for block-Jacobi DIC (ldu_dic_setup, dic_*_solve; readings
+Z35-Z36) against oracle.dic_pcg(bounds=...).
 """
 import json
 import os
@@ -32,6 +34,7 @@ def main():
     uid = [ldu.Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = ldu.Comm(rank, world, uid[0], local)
+    dic = len(sys.argv) > 1 and sys.argv[1] == "dic"
     cases = {
         "hex": lambda: meshgen.hex_laplacian(24, 20, 32, dirichlet=dict(x0=1.0)),
         "hex_sigma": lambda: meshgen.hex_laplacian(21, 17, 19, conductance_sigma=0.6, seed=3,
@@ -46,11 +49,18 @@ def main():
         bounds = meshgen.slab_bounds(g.nCells, world)
         lo, hi = int(bounds[rank]), int(bounds[rank + 1])
         A = ldu.LduMatrix.from_system(parts[rank], comm)
-        info = A.amg_setup()
-        out = {"sizes": info["n"], "agg0": A.amg_aggregates(0) if info["nLevels"] else None}
+        if dic:
+            A.dic_setup()
+            out = {}
+        else:
+            info = A.amg_setup()
+            out = {"sizes": info["n"], "agg0": A.amg_aggregates(0) if info["nLevels"] else None}
         b = torch.from_numpy(g.b[lo:hi].copy()).cuda()
         for solver in ("pcg", "pipecg"):
-            fn = A.amg_pcg_solve if solver == "pcg" else A.amg_pipecg_solve
+            if dic:
+                fn = A.dic_pcg_solve if solver == "pcg" else A.dic_pipecg_solve
+            else:
+                fn = A.amg_pcg_solve if solver == "pcg" else A.amg_pipecg_solve
             x = torch.zeros_like(b)
             st, it, res = fn(b, x, tol=1e-10, maxIter=500)
             reds = A.stats()["allreduces"]
@@ -64,18 +74,28 @@ def main():
         gathered = [None] * world
         dist.all_gather_object(gathered, out)
         if rank == 0:
+            import oracle
             from oracle import amg
-            Hs = amg.block_hierarchies(parts)
-            r = {"sizes_ok": all(gathered[k]["sizes"] == Hs[k].sizes for k in range(world))}
-            ok &= r["sizes_ok"]
-            ok &= all(gathered[k]["agg0"] is None or np.array_equal(gathered[k]["agg0"], Hs[k].levels[0].agg)
-                      for k in range(world))
+            if dic:
+                r = {}
+            else:
+                Hs = amg.block_hierarchies(parts)
+                r = {"sizes_ok": all(gathered[k]["sizes"] == Hs[k].sizes for k in range(world))}
+                ok &= r["sizes_ok"]
+                ok &= all(gathered[k]["agg0"] is None or np.array_equal(gathered[k]["agg0"], Hs[k].levels[0].agg)
+                          for k in range(world))
             for solver in ("pcg", "pipecg"):
                 pip = solver == "pipecg"
-                ost, ox, oit, ores = amg.amg_block_solve(g, g.b, bounds, Hs, tol=1e-10,
-                                                         maxIter=500, pipelined=pip)
-                _, _, _, _, ohist = amg.amg_block_solve(g, g.b, bounds, Hs, tol=0.0, maxIter=6,
-                                                        pipelined=pip, history=True)
+                if dic:
+                    ost, ox, oit, ores = oracle.dic_pcg(g, g.b, tol=1e-10, maxIter=500,
+                                                        pipelined=pip, bounds=bounds)
+                    _, _, _, _, ohist = oracle.dic_pcg(g, g.b, tol=0.0, maxIter=6, pipelined=pip,
+                                                       bounds=bounds, history=True)
+                else:
+                    ost, ox, oit, ores = amg.amg_block_solve(g, g.b, bounds, Hs, tol=1e-10,
+                                                             maxIter=500, pipelined=pip)
+                    _, _, _, _, ohist = amg.amg_block_solve(g, g.b, bounds, Hs, tol=0.0,
+                                                            maxIter=6, pipelined=pip, history=True)
                 sts = {o[solver][0] for o in gathered}
                 its = {o[solver][1] for o in gathered}
                 it = gathered[0][solver][1]

@@ -46,3 +46,15 @@ def test_distributed_amg_parity(nproc):
            os.path.join(ROOT, "tests", "dist_amg_worker.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert p.returncode == 0 and "DIST_AMG_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_distributed_dic_parity(nproc):
+    """Block-Jacobi DIC-PCG / DIC-PipeCG across ranks (readings Z33, Z35) = the oracle's block DIC."""
+    if _ngpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", "--master-port=29535",
+           os.path.join(ROOT, "tests", "dist_amg_worker.py"), "dic"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0 and "DIST_AMG_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
