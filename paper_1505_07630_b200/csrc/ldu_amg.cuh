@@ -101,6 +101,12 @@ struct DicFactor {
   int nPad = 0;                  // padded positions
   unsigned* flag = nullptr;      // [n] per-cell epoch tag of the sync-free sweeps
   unsigned* ctl = nullptr;       // [3] epoch, forward ticket, backward ticket
+  // ELL copy of the same rows (width = the largest row, padded with column -1), [w][nPad]
+  // position-major so one level's rows are contiguous; used when the width is <= 8
+  int wLo = 0, wUp = 0;
+  int* dLevPtr = nullptr;        // device copy of levPtr (runs of narrow levels in one block)
+  int *eLoCol = nullptr, *eUpCol = nullptr;
+  double *eLoVal = nullptr, *eUpVal = nullptr;
   long long nnzL = 0;
   int maxLevel = 0;              // cells in the widest level
 };

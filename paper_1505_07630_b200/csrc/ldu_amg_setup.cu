@@ -1133,7 +1133,9 @@ void amg_release(ldu_handle h) {
   H->Ac.release();
   DicFactor& D = H->dic;
   for (void* p : {(void*)D.perm, (void*)D.loPtr, (void*)D.loCol, (void*)D.loVal, (void*)D.upPtr,
-                  (void*)D.upCol, (void*)D.upVal, (void*)D.rD, (void*)D.flag, (void*)D.ctl})
+                  (void*)D.upCol, (void*)D.upVal, (void*)D.rD, (void*)D.flag, (void*)D.ctl,
+                  (void*)D.eLoCol, (void*)D.eUpCol, (void*)D.eLoVal, (void*)D.eUpVal,
+                  (void*)D.dLevPtr})
     dfree(p);
   for (void* p : {(void*)H->Ainv, (void*)H->fL, (void*)H->zL, (void*)H->u, (void*)H->m,
                   (void*)H->zk, (void*)H->qk})
@@ -1417,6 +1419,29 @@ void dic_setup(ldu_handle h) {
     }
     lp[nPad] = (int)ol;
     up[nPad] = (int)ou;
+    // ELL copies (position-major) when the rows are short
+    auto ell = [&](const std::vector<int>& P, const std::vector<int>& C, const std::vector<double>& V,
+                   int& w, int*& dc, double*& dv) {
+      int W = 0;
+      for (int k = 0; k < nPad; ++k) W = std::max(W, P[k + 1] - P[k]);
+      w = W;
+      if (W == 0 || W > 8) return;
+      std::vector<int> ec((size_t)W * nPad, -1);
+      std::vector<double> ev((size_t)W * nPad, 0.0);
+      for (int k = 0; k < nPad; ++k)
+        for (int j = P[k]; j < P[k + 1]; ++j) {
+          ec[(size_t)(j - P[k]) * nPad + k] = C[j];
+          ev[(size_t)(j - P[k]) * nPad + k] = V[j];
+        }
+      dc = dmalloc<int>((size_t)W * nPad);
+      dv = dmalloc<double>((size_t)W * nPad);
+      CUDA_CHECK(cudaMemcpy(dc, ec.data(), sizeof(int) * ec.size(), cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(dv, ev.data(), sizeof(double) * ev.size(), cudaMemcpyHostToDevice));
+    };
+    D.dLevPtr = dmalloc<int>(nLev + 1);
+    CUDA_CHECK(cudaMemcpy(D.dLevPtr, D.levPtr.data(), sizeof(int) * (nLev + 1), cudaMemcpyHostToDevice));
+    ell(lp, lc, lvv, D.wLo, D.eLoCol, D.eLoVal);
+    ell(up, uc, uvv, D.wUp, D.eUpCol, D.eUpVal);
     D.perm = dmalloc<int>(nPad);
     D.loPtr = dmalloc<int>(nPad + 1);
     D.loCol = dmalloc<int>(std::max(1LL, nnzL));

@@ -505,6 +505,123 @@ __global__ void k_dic_bump(unsigned* ctl, const State* st) {
   ctl[2] = 0u;
 }
 
+// ELL sweeps with programmatic dependent launch: the level's row data (constant since the setup)
+// is loaded before griddepcontrol.wait, so it overlaps the previous level's execution and the
+// launch gap; f and z (produced by earlier kernels) are read only after the wait.  The grid covers the
+// level exactly.  W = padded row width (column -1 = no entry).
+template <int W, bool FWD>
+__global__ void __launch_bounds__(kBlock) k_dic_ell(int beg, int end, int nPad,
+                                                    const int* __restrict__ perm,
+                                                    const int* __restrict__ ecol,
+                                                    const double* __restrict__ eval,
+                                                    const double* __restrict__ rD,
+                                                    const double* f, double* z, const State* st) {
+  const int k = beg + blockIdx.x * blockDim.x + threadIdx.x;
+  int c = -1;
+  int cj[W];
+  double a[W];
+  double rc = 0.0;
+  if (k < end) {
+    c = __ldg(perm + k);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      cj[w] = __ldg(ecol + (size_t)w * nPad + k);
+      a[w] = __ldg(eval + (size_t)w * nPad + k);
+    }
+    if (c >= 0) rc = __ldg(rD + c);
+  }
+  pdl_wait();     // the previous level (and, transitively, every earlier kernel) is complete
+  pdl_trigger();  // after the wait: at most one level of look-ahead is resident
+  if ((st && st->done) || c < 0) return;
+  double s = FWD ? f[c] : 0.0;
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+    if (cj[w] >= 0) s = FWD ? fma(-a[w], z[cj[w]], s) : fma(a[w], z[cj[w]], s);
+  if (FWD)
+    z[c] = rc * s;
+  else if (cj[0] >= 0)
+    z[c] = fma(-rc, s, z[c]);
+}
+
+// A run of consecutive narrow levels (each <= kRun positions) in ONE block: __syncthreads between
+// levels (global writes before the barrier are visible to the block after it) instead of a launch
+// per level.  Levels [l0, l1) ascending (FWD) or descending (!FWD).
+constexpr int kRun = 1024;
+template <int W, bool FWD>
+__global__ void __launch_bounds__(kRun) k_dic_ell_run(int l0, int l1, const int* __restrict__ levPtr,
+                                                      int nPad, const int* __restrict__ perm,
+                                                      const int* __restrict__ ecol,
+                                                      const double* __restrict__ eval,
+                                                      const double* __restrict__ rD,
+                                                      const double* f, double* z, const State* st) {
+  pdl_wait();
+  pdl_trigger();
+  if (st && st->done) return;
+  for (int i = 0; i < l1 - l0; ++i) {
+    const int l = FWD ? l0 + i : l1 - 1 - i;
+    const int k = __ldg(levPtr + l) + threadIdx.x;
+    if (k < __ldg(levPtr + l + 1)) {
+      const int c = __ldg(perm + k);
+      if (c >= 0) {
+        double s = FWD ? f[c] : 0.0;
+        bool any = false;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const int cj = __ldg(ecol + (size_t)w * nPad + k);
+          if (cj >= 0) {
+            const double a = __ldg(eval + (size_t)w * nPad + k);
+            s = FWD ? fma(-a, z[cj], s) : fma(a, z[cj], s);
+            any = true;
+          }
+        }
+        if (FWD)
+          z[c] = __ldg(rD + c) * s;
+        else if (any)
+          z[c] = fma(-__ldg(rD + c), s, z[c]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <bool FWD>
+void launch_dic_run(int W, bool pdl, int l0, int l1, const int* levPtr, int nPad, const int* perm,
+                    const int* ecol, const double* eval, const double* rD, const double* f,
+                    double* z, const State* st, cudaStream_t s) {
+#define LDU_DIC_RUN(WW)                                                                          \
+  launch_pdl(pdl, k_dic_ell_run<WW, FWD>, 1, kRun, s, l0, l1, levPtr, nPad, perm, ecol, eval, rD, \
+             f, z, st);                                                                          \
+  return;
+  switch (W) {
+    case 1: LDU_DIC_RUN(1)
+    case 2: LDU_DIC_RUN(2)
+    case 3: LDU_DIC_RUN(3)
+    case 4: LDU_DIC_RUN(4)
+    case 5: case 6: LDU_DIC_RUN(6)
+    default: LDU_DIC_RUN(8)
+  }
+#undef LDU_DIC_RUN
+}
+
+template <bool FWD>
+void launch_dic_ell(int W, bool pdl, int b, int e, int nPad, const int* perm, const int* ecol,
+                    const double* eval, const double* rD, const double* f, double* z,
+                    const State* st, cudaStream_t s) {
+  const int g = std::max(1, (e - b + kBlock - 1) / kBlock);
+#define LDU_DIC_ELL(WW)                                                                         \
+  launch_pdl(pdl, k_dic_ell<WW, FWD>, g, kBlock, s, b, e, nPad, perm, ecol, eval, rD, f, z, st); \
+  return;
+  switch (W) {
+    case 1: LDU_DIC_ELL(1)
+    case 2: LDU_DIC_ELL(2)
+    case 3: LDU_DIC_ELL(3)
+    case 4: LDU_DIC_ELL(4)
+    case 5: case 6: LDU_DIC_ELL(6)
+    default: LDU_DIC_ELL(8)
+  }
+#undef LDU_DIC_ELL
+}
+
 long long enqueue_dic(ldu_handle h, const double* f0, double* z0, cudaStream_t s, State* st,
                       const Red* rho) {
   const DicFactor& D = h->amg->dic;
@@ -513,7 +630,45 @@ long long enqueue_dic(ldu_handle h, const double* f0, double* z0, cudaStream_t s
   // LDU_DIC_SF = back-off in ns of the sync-free sweeps (0 = one launch per level, the default)
   static const int sf = std::getenv("LDU_DIC_SF") ? std::atoi(std::getenv("LDU_DIC_SF")) : 0;
   static const int sfBlocks = std::getenv("LDU_DIC_SF_BLOCKS") ? std::atoi(std::getenv("LDU_DIC_SF_BLOCKS")) : 148 * 4;
-  if (!sf) {  // one launch per level and sweep (measured reference variant)
+  static const bool useEll = !(std::getenv("LDU_DIC_ELL") && std::atoi(std::getenv("LDU_DIC_ELL")) == 0);
+  static const bool ellPdl = !(std::getenv("LDU_DIC_PDL") && std::atoi(std::getenv("LDU_DIC_PDL")) == 0);
+  if (!sf && useEll && D.eLoCol && (D.nLev < 2 || D.eUpCol)) {
+    // one launch per level and sweep, ELL rows, PDL between consecutive launches (default).
+    // LDU_DIC_RUN = m > 0: runs of >= m narrow levels (<= kRun positions) in one single-block
+    // launch each -- measured slower inside the solver's graphs (profiles/r01_dic), so opt-in
+    static const int minRun = std::getenv("LDU_DIC_RUN") ? std::atoi(std::getenv("LDU_DIC_RUN")) : 0;
+    auto narrow = [&](int l) { return D.levPtr[l + 1] - D.levPtr[l] <= kRun; };
+    long long launches = 0;
+    for (int l = 0; l < D.nLev;) {  // forward, levels ascending
+      int e = l;
+      while (minRun > 0 && e < D.nLev && narrow(e)) ++e;
+      if (e - l >= minRun) {
+        launch_dic_run<true>(D.wLo, ellPdl && launches > 0, l, e, D.dLevPtr, D.nPad, D.perm,
+                             D.eLoCol, D.eLoVal, D.rD, f0, z0, st, s);
+        l = e;
+      } else {
+        launch_dic_ell<true>(D.wLo, ellPdl && launches > 0, D.levPtr[l], D.levPtr[l + 1], D.nPad,
+                             D.perm, D.eLoCol, D.eLoVal, D.rD, f0, z0, st, s);
+        ++l;
+      }
+      ++launches;
+    }
+    for (int l = D.nLev - 2; l >= 0;) {  // backward, levels descending
+      int b = l;
+      while (minRun > 0 && b >= 0 && narrow(b)) --b;
+      if (l - b >= minRun) {
+        launch_dic_run<false>(D.wUp, ellPdl, b + 1, l + 1, D.dLevPtr, D.nPad, D.perm, D.eUpCol,
+                              D.eUpVal, D.rD, f0, z0, st, s);
+        l = b;
+      } else {
+        launch_dic_ell<false>(D.wUp, ellPdl, D.levPtr[l], D.levPtr[l + 1], D.nPad, D.perm,
+                              D.eUpCol, D.eUpVal, D.rD, f0, z0, st, s);
+        --l;
+      }
+      ++launches;
+    }
+    kernels += launches;
+  } else if (!sf) {  // one launch per level and sweep, CSR rows (measured reference variant)
     for (int l = 0; l < D.nLev; ++l) {
       const int b = D.levPtr[l], e = D.levPtr[l + 1];
       k_dic_fwd<<<grid(e - b), kBlock, 0, s>>>(b, e, D.perm, D.loPtr, D.loCol, D.loVal, D.rD, f0,
