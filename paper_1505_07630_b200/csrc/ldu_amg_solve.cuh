@@ -642,7 +642,7 @@ long long enqueue_dic(ldu_handle h, const double* f0, double* z0, cudaStream_t s
     for (int l = 0; l < D.nLev;) {  // forward, levels ascending
       int e = l;
       while (minRun > 0 && e < D.nLev && narrow(e)) ++e;
-      if (e - l >= minRun) {
+      if (minRun > 0 && e - l >= minRun) {
         launch_dic_run<true>(D.wLo, ellPdl && launches > 0, l, e, D.dLevPtr, D.nPad, D.perm,
                              D.eLoCol, D.eLoVal, D.rD, f0, z0, st, s);
         l = e;
@@ -656,7 +656,7 @@ long long enqueue_dic(ldu_handle h, const double* f0, double* z0, cudaStream_t s
     for (int l = D.nLev - 2; l >= 0;) {  // backward, levels descending
       int b = l;
       while (minRun > 0 && b >= 0 && narrow(b)) --b;
-      if (l - b >= minRun) {
+      if (minRun > 0 && l - b >= minRun) {
         launch_dic_run<false>(D.wUp, ellPdl, b + 1, l + 1, D.dLevPtr, D.nPad, D.perm, D.eUpCol,
                               D.eUpVal, D.rD, f0, z0, st, s);
         l = b;
