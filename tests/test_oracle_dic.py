@@ -150,3 +150,19 @@ def test_dic_zero_rhs_and_nonpositive_pivot():
                             np.array([1.0, 1.0]), np.array([-2.0]), None, np.ones(2))
     st, _, _ = oracle.dic(bad)
     assert st == oracle.BREAKDOWN
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_dic_block_form_equals_per_rank_local_factors(p):
+    """The multi-rank reading (Z33 applied to DIC): the block form over the slab bounds is the DIC
+    of each rank's LOCAL matrix, as meshgen.slab_partition hands it to ldu_setup."""
+    g = meshgen.hex_laplacian(7, 6, 9, conductance_sigma=0.4, seed=2)
+    parts = meshgen.slab_partition(g, p)
+    bounds = meshgen.slab_bounds(g.nCells, p)
+    r = meshgen.rhs_random(g.nCells, seed=3)
+    _, rD, w = oracle.dic(g, r, bounds=bounds)
+    for k, part in enumerate(parts):
+        lo, hi = int(bounds[k]), int(bounds[k + 1])
+        _, rDk, wk = oracle.dic(part, r[lo:hi])
+        np.testing.assert_allclose(rD[lo:hi], rDk, rtol=1e-14)
+        np.testing.assert_allclose(w[lo:hi], wk, rtol=1e-12, atol=1e-14)
