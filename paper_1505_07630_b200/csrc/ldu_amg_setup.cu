@@ -1424,8 +1424,12 @@ void dic_setup(ldu_handle h) {
                    int& w, int*& dc, double*& dv) {
       int W = 0;
       for (int k = 0; k < nPad; ++k) W = std::max(W, P[k + 1] - P[k]);
+      if (W == 0 || W > 8) {
+        w = W;
+        return;
+      }
+      W = W <= 4 ? W : (W <= 6 ? 6 : 8);  // the widths the sweep kernels are instantiated for
       w = W;
-      if (W == 0 || W > 8) return;
       std::vector<int> ec((size_t)W * nPad, -1);
       std::vector<double> ev((size_t)W * nPad, 0.0);
       for (int k = 0; k < nPad; ++k)
