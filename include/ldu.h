@@ -284,6 +284,8 @@ typedef struct {
   int widestLevel;          /* cells in the widest level                                          */
   long long lowerEntries;   /* stored strictly-lower couplings (non-zero)                         */
   double setupMs;           /* device + host time of ldu_dic_setup                                */
+  int ellWidthLower;        /* padded ELL width of the forward-sweep rows (0 = CSR rows used)     */
+  int ellWidthUpper;        /* padded ELL width of the backward-sweep rows (0 = CSR rows used)    */
 } ldu_dic_info;
 
 ldu_status ldu_dic_setup(ldu_handle h);

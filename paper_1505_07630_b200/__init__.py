@@ -115,7 +115,8 @@ class AmgInfo(ctypes.Structure):
 class DicInfo(ctypes.Structure):
     """ldu_dic_info (include/ldu.h)."""
     _fields_ = [("nLevels", ctypes.c_int), ("widestLevel", ctypes.c_int),
-                ("lowerEntries", ctypes.c_longlong), ("setupMs", ctypes.c_double)]
+                ("lowerEntries", ctypes.c_longlong), ("setupMs", ctypes.c_double),
+                ("ellWidthLower", ctypes.c_int), ("ellWidthUpper", ctypes.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

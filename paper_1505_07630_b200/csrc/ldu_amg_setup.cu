@@ -1505,6 +1505,8 @@ void dic_export(ldu_handle h, double* rD, ldu_dic_info* info) {
     info->widestLevel = H->dic.maxLevel;
     info->lowerEntries = H->dic.nnzL;
     info->setupMs = H->setupMs;
+    info->ellWidthLower = H->dic.eLoCol ? H->dic.wLo : 0;
+    info->ellWidthUpper = H->dic.eUpCol ? H->dic.wUp : 0;
   }
 }
 

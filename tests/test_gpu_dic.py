@@ -69,6 +69,38 @@ def test_dic_factor_and_apply(ldu, case):
             assert info["nLevels"] == 300 and info["widestLevel"] == 1
 
 
+def star_chain(hubs):
+    """40-cell chain plus extra faces {k -> hub}: hub rows with len(ks)+1 lower entries."""
+    n = 40
+    l = list(range(n - 1))
+    u = list(range(1, n))
+    for hub, ks in hubs.items():
+        l += ks
+        u += [hub] * len(ks)
+    l, u = np.array(l, np.int32), np.array(u, np.int32)
+    a = -np.linspace(0.5, 1.5, l.shape[0])
+    diag = np.bincount(l, np.abs(a), n) + np.bincount(u, np.abs(a), n) + 1.0
+    return meshgen.LduSystem(n, l, u, diag, a, None, np.ones(n))
+
+
+@pytest.mark.parametrize("hubs,wlo", [({30: [1, 2, 3, 4]}, 6),            # width 5 -> kernel 6
+                                      ({39: [0, 5, 10, 15, 20, 25]}, 8),  # width 7 -> kernel 8
+                                      ({39: list(range(0, 32, 4))}, 0)])  # width 9 -> CSR rows
+def test_dic_ell_widths(ldu, hubs, wlo):
+    sys_ = star_chain(hubs)
+    r = meshgen.rhs_random(sys_.nCells, seed=4)
+    _, rD_o, w_o = oracle.dic(sys_, r)
+    with ldu.LduMatrix.from_system(sys_) as A:
+        info = A.dic_setup()
+        assert info["ellWidthLower"] == wlo, info
+        np.testing.assert_allclose(A.dic_rD(np.empty(sys_.nCells)), rD_o, rtol=1e-12)
+        assert rel(A.dic_apply(r, np.empty(sys_.nCells)), w_o) <= 1e-12
+        x = np.zeros(sys_.nCells)
+        st, it, _ = A.dic_pcg_solve(sys_.b, x, tol=1e-10, maxIter=200)
+        ost, ox, oit, _ = oracle.dic_pcg(sys_, sys_.b, tol=1e-10, maxIter=200)
+        assert st == ldu.OK and abs(it - oit) <= 1 and rel(x, ox) <= 1e-8
+
+
 @pytest.mark.parametrize("case", ["hex16", "hex_ragged", "cavity", "irregular"])
 @pytest.mark.parametrize("pipelined", [False, True])
 def test_dic_solve_parity(ldu, case, pipelined):
