@@ -88,6 +88,47 @@ def pass_format_bytes(solver, info, N):
     return base + 12 * info["storedEntries"] + 12 * ((N + 31) // 32)
 
 
+def iter_format_bytes(solver, info, N, P):
+    """Bytes one iteration must move in the layout and pass structure actually run: the fused
+    pipelined pass alone; classical = pass A (A1 + A2) + pass B (r, q, rD in; r out: 32N);
+    plus the halo (faceCells 4 + coeffs 8 + send 8 + recv 8 per interface face)."""
+    b = pass_format_bytes(solver, info, N)
+    if solver == "pcg":
+        b += 32 * N
+    elif not info.get("pipeFused"):
+        b += 24 * N + 8 * (info["nDiagonals"] if info["layout_name"] == "DIA_SYM" else 0) * N
+    return b + 28 * P
+
+
+def host_cpu():
+    """The host the CPU oracle runs on (record nproc and the lscpu model)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
+def pinned_to_one_core(fn):
+    """Run fn with this process pinned to one core (the `taskset -c <core>` of SURVEY §8(d))."""
+    try:
+        old = os.sched_getaffinity(0)
+        core = min(old)
+        os.sched_setaffinity(0, {core})
+    except Exception:
+        old, core = None, None
+    try:
+        return fn(), core
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+
+
 def vcycle_bytes(amg, info):
     """Bytes one V-cycle must move in the layouts it streams: level 0 on the
     handle's DIA layout (nd coefficient arrays), coarser levels and every P / R as CSR (12 B per
@@ -305,6 +346,8 @@ def main():
         dist.all_reduce(tot)
     Ng, Fg, Pg = (float(v) for v in tot.tolist())
     peak, peak_src = hbm_peak()
+    # the paper's STREAM-measured roofline: our fp64 triad, same run, same device
+    triad = ldu.stream_triad(local, 1 << 28, 5)
 
     def timed(solver, sample_clocks):
         """W warm-up solves, then K timed solves bracketed by barrier + synchronize; device time
@@ -363,18 +406,28 @@ def main():
             mb = pass_model_bytes(solver, N, F, fused)
             fb = pass_format_bytes(solver, info, N)
             kname = ("k_cg_passA1+k_cg_passA2" if info.get("variant") == 7 else "k_cg_passA")
+            # achieved / frac: the bytes the layout must move per launch over the
+            # live launch time; the §8(d) LDU-model figure is reported only as the labelled
+            # "model-equivalent" rate (it counts int32 addressing and unfused passes the DIA
+            # layout and the fused pass never move, so it can exceed the copy peak)
             roof = {"kernel": kname if solver == "pcg" else ("k_pipe_SU" if fused else "k_pipe_U"),
-                    "bound": "hbm", "achieved": mb / t_launch / 1e9, "peak": peak, "unit": "GB/s",
-                    "frac": mb / t_launch / 1e9 / peak, "traffic": ncu_traffic(solver, n, world),
-                    "model_bytes_per_launch": mb, "launch_us": t_launch * 1e6,
-                    "format_bytes_per_launch": fb, "format_achieved": fb / t_launch / 1e9,
-                    "format_frac": fb / t_launch / 1e9 / peak, "peak_source": peak_src,
+                    "bound": "hbm", "achieved": fb / t_launch / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": fb / t_launch / 1e9 / peak, "traffic": ncu_traffic(solver, n, world),
+                    "bytes_per_launch": fb, "launch_us": t_launch * 1e6,
+                    "triad_frac": (fb / t_launch / 1e9 / triad) if triad else None,
+                    "model_bytes_per_launch": mb,
+                    "model_equivalent_gbps": mb / t_launch / 1e9, "peak_source": peak_src,
                     "share_of_step": pass_ms / 1e3 / prof["elapsed"],
                     "timed_with_event_nodes_ms_per_step": 1e3 * prof["elapsed"] / args.steps}
         bytes_iter = model_bytes(solver, Ng, Fg, Pg)
+        fb_iter = torch.tensor([float(iter_format_bytes(solver, info, N, P))], dtype=torch.float64,
+                               device="cuda")
+        if dist is not None:
+            dist.all_reduce(fb_iter)
+        fb_iter = float(fb_iter.item())
         return dict(value=value, elapsed=elapsed, kernels=kernels, roof=roof, clk=clk,
-                    status=int(st), iters=it, bytes_iter=bytes_iter,
-                    eff=value * bytes_iter / 1e9)
+                    status=int(st), iters=it, bytes_iter=bytes_iter, fb_iter=fb_iter,
+                    eff=value * fb_iter / 1e9, model_eff=value * bytes_iter / 1e9)
 
     main_r = timed(args.solver, True)
     value, elapsed, kernels = main_r["value"], main_r["elapsed"], main_r["kernels"]
@@ -386,8 +439,10 @@ def main():
         r2 = timed(other, False)
         secondary = {"solver": other, "value": r2["value"], "unit": UNIT,
                      "ms_per_step": 1e3 * r2["elapsed"] / args.steps,
-                     "effective_gbps": r2["eff"], "bytes_per_iter_model": r2["bytes_iter"],
-                     "effective_frac_of_hbm": r2["eff"] / (peak * world), "roofline": r2["roof"]}
+                     "effective_gbps": r2["eff"], "bytes_per_iter": r2["fb_iter"],
+                     "effective_frac_of_hbm": r2["eff"] / (peak * world),
+                     "model_bytes_per_iter": r2["bytes_iter"],
+                     "model_equivalent_gbps": r2["model_eff"], "roofline": r2["roof"]}
     solve = A.pcg_solve if args.solver == "pcg" else A.pipecg_solve
 
     # end to end through the public API with host buffers (pinned), copies inside the timed region
@@ -461,6 +516,8 @@ def main():
                "operator_complexity": ai["operatorComplexity"],
                "jacobi_pcg": {"iterations": jit, "ms_per_solve": 1e3 * t_jac, "status": int(jst)},
                "time_to_solution_speedup_vs_jacobi_pcg": t_jac / t_amg,
+               "setup_plus_solve_ms": ai["setupMs"] + 1e3 * t_amg,
+               "speedup_vs_jacobi_pcg_incl_setup": t_jac / (t_amg + ai["setupMs"] / 1e3),
                "gpu_launches_per_solve": akern // args.steps,
                "vcycle": {"ms": vc_ms, "krylov_passes_ms": kr_ms, "bytes": vb,
                           "achieved": vb / (vc_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
@@ -470,11 +527,13 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         k1, k2 = 3, 15
-        rate, per = oracle_iter_rate(sys_, sys_.b, args.solver, k1, k2)
+        (rate, per), core = pinned_to_one_core(
+            lambda: oracle_iter_rate(sys_, sys_.b, args.solver, k1, k2))
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"oracle {args.solver} (C, fp64, -O2, 1 thread) on the same {n}^3 system: "
-                         f"(t({k2} it) - t({k1} it)) / {k2 - k1}",
-               "effective_gbps": rate * bytes_iter / 1e9}
+               "sample": f"oracle {args.solver} (C, fp64, -O2, 1 thread, pinned to core {core}) on "
+                         f"the same {n}^3 system: (t({k2} it) - t({k1} it)) / {k2 - k1}",
+               "host": host_cpu(), "pinned_core": core,
+               "model_equivalent_gbps": rate * bytes_iter / 1e9}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -482,9 +541,11 @@ def main():
                "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": config_dict(args, world, info),
-               "effective_gbps": value * bytes_iter / 1e9,
-               "effective_frac_of_hbm": value * bytes_iter / 1e9 / (peak * world),
-               "bytes_per_iter_model": bytes_iter,
+               "effective_gbps": main_r["eff"],
+               "effective_frac_of_hbm": main_r["eff"] / (peak * world),
+               "bytes_per_iter": main_r["fb_iter"],
+               "model_bytes_per_iter": bytes_iter, "model_equivalent_gbps": main_r["model_eff"],
+               "stream_triad_gbps": triad, "hbm_peak_gbps": peak, "hbm_peak_source": peak_src,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels,
                "secondary": secondary, "amg": amg,
                "clocks": clk, "last_status": int(st), "iterations_per_step": it}

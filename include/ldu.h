@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define LDU_ABI_VERSION 1
+#define LDU_ABI_VERSION 2
 
 typedef enum {
   LDU_OK = 0,                /* converged: finalRes < tol (or r == 0 exactly; reading Z2)         */
@@ -75,6 +75,20 @@ ldu_status ldu_get_unique_id(void *id128);
 /* Creates the rank's communicators (one for reductions, one for halo exchange) on cudaDevice.
  * Collective over nRanks processes.  Errors: INVALID_ARG, CUDA, NCCL. */
 ldu_status ldu_comm_init(int rank, int nRanks, const void *id128, int cudaDevice, ldu_comm *out);
+
+/* Host bootstrap of a communicator without NCCL: every exchange inside the library (halo values
+ * and the fused reductions) then runs over the peer-memory mailboxes only, and the
+ * one-time setup exchange (CUDA IPC handles + interface tables) and setup barriers go through
+ * the caller's host all-gather `fn`:
+ *     fn(ctx, send, recv, bytes) gathers `bytes` bytes from every rank into recv[nRanks * bytes]
+ *     in rank order (host memory) and returns 0 on success.
+ * (e.g. torch.distributed over gloo: plumbing only, never called inside a solve.)  Unlike NCCL
+ * this allows several ranks on ONE device (processes sharing a GPU through CUDA IPC), which is
+ * how the multi-rank path is parity-tested on a single-GPU box.  The function pointer and ctx
+ * must stay valid until ldu_comm_destroy.  Errors: INVALID_ARG, CUDA. */
+typedef int (*ldu_host_allgather_fn)(void *ctx, const void *send, void *recv, unsigned long long bytes);
+ldu_status ldu_comm_init_host(int rank, int nRanks, int cudaDevice, ldu_host_allgather_fn fn,
+                              void *ctx, ldu_comm *out);
 ldu_status ldu_comm_destroy(ldu_comm comm);
 
 /* ---- setup ------------------------------------------------------------- */
@@ -103,8 +117,11 @@ ldu_status ldu_setup(int nCells, int nFaces, const int *lowerAddr, const int *up
                      const double *diag, const double *lower, const double *upper,
                      const ldu_interfaces *interfaces, ldu_handle *out);
 
-/* Work stream for all subsequent calls on h (e.g. torch.cuda.current_stream().cuda_stream).
- * NULL restores the handle's own stream.  The solves still return only after completion. */
+/* The caller's stream for all subsequent calls on h (e.g. torch.cuda.current_stream().cuda_stream):
+ * every call orders its device work after the work already enqueued on that stream (device
+ * inputs written there are safe to read) and that stream's later work after the call's.  NULL
+ * (the default) = the legacy default stream, CUDA stream 0.  The library computes on its own
+ * streams; the solves still return only after completion. */
 ldu_status ldu_set_stream(ldu_handle h, void *cudaStream);
 
 /* y = A x including processor interfaces ("point-to-point communication during the
@@ -164,12 +181,17 @@ typedef struct {
   double solveMs;        /* device time of the last solve (CUDA events, whole call)            */
   double iterMs;         /* device time of its iteration loop only (excludes r0 and finalize)  */
   long long kernels;     /* kernel launches of this library in the last call (graph nodes incl.) */
-  long long allreduces;  /* global reductions issued in the last solve (per rank)              */
+  long long allreduces;  /* cross-rank reductions completed in the last solve (per rank; 0 on one
+                            rank): counted ON THE DEVICE by the control step that consumes each
+                            gathered set of sums (reading Z4 / P:97: 2 per classical iteration,
+                            1 per pipelined iteration, plus the r0 reductions)                  */
   long long haloBytes;   /* halo bytes sent by this rank in the last call                      */
   long long h2dBytes;    /* host->device bytes copied for b/x in the last call                 */
   long long d2hBytes;    /* device->host bytes copied for x in the last call                   */
   int iterations;        /* nIter of the last solve                                            */
-  int reserved;
+  int reductions;        /* global (grid-wide, and cross-rank when multi-rank) reductions whose
+                            sums were consumed by a control step in the last solve, counted on
+                            the device; single rank included                                     */
   double passMs[2];      /* profile = 1: summed device time of pass 0 (classical A / pipelined S)
                             and pass 1 (classical B / pipelined U) over all iterations           */
   long long passLaunches[2]; /* number of timed launches of each pass                          */

@@ -60,11 +60,11 @@ class SolveStats(ctypes.Structure):
                 ("kernels", ctypes.c_longlong), ("allreduces", ctypes.c_longlong),
                 ("haloBytes", ctypes.c_longlong), ("h2dBytes", ctypes.c_longlong),
                 ("d2hBytes", ctypes.c_longlong), ("iterations", ctypes.c_int),
-                ("reserved", ctypes.c_int), ("passMs", ctypes.c_double * 2),
+                ("reductions", ctypes.c_int), ("passMs", ctypes.c_double * 2),
                 ("passLaunches", ctypes.c_longlong * 2)]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
         d["passMs"] = list(self.passMs)
         d["passLaunches"] = list(self.passLaunches)
         return d
@@ -133,6 +133,7 @@ SIGNATURES = {
     "ldu_last_error": (ctypes.c_char_p, []),
     "ldu_get_unique_id": (_S, [_P]),
     "ldu_comm_init": (_S, [_I, _I, _P, _I, ctypes.POINTER(_P)]),
+    "ldu_comm_init_host": (_S, [_I, _I, _I, _P, _P, ctypes.POINTER(_P)]),
     "ldu_comm_destroy": (_S, [_P]),
     "ldu_setup": (_S, [_I, _I, _P, _P, _P, _P, _P, ctypes.POINTER(_Interfaces), ctypes.POINTER(_P)]),
     "ldu_set_stream": (_S, [_P, _P]),
@@ -203,17 +204,52 @@ def _len(a) -> int:
     return int(a.shape[0])
 
 
-class Comm:
-    """Two NCCL communicators (reductions, halo) for one rank -- ldu_comm_init."""
+_HostAllgather = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_ulonglong)
 
-    def __init__(self, rank: int, nranks: int, unique_id: bytes, device: int):
-        if len(unique_id) != 128:
-            raise ValueError("unique id must be 128 bytes")
-        self._id = ctypes.create_string_buffer(unique_id, 128)
+
+class Comm:
+    """One rank's communicator.  ``Comm(rank, n, uid, device)``: two NCCL communicators
+    (ldu_comm_init).  ``Comm.host(rank, n, device, group)``: no NCCL -- every exchange runs over
+    the peer-memory mailboxes and the one-time setup exchange goes through torch.distributed on
+    ``group`` (gloo), so several ranks may share one GPU (ldu_comm_init_host)."""
+
+    def __init__(self, rank: int, nranks: int, unique_id: Optional[bytes], device: int,
+                 _host_group=None):
         h = _P()
-        _check(_lib.ldu_comm_init(rank, nranks, self._id, device, ctypes.byref(h)))
+        self._cb = None
+        if unique_id is None:
+            import torch
+            import torch.distributed as dist
+            group = _host_group
+
+            def _allgather(ctx, send, recv, nbytes):  # plumbing: bytes in, bytes out
+                try:
+                    src = torch.frombuffer(bytearray(ctypes.string_at(send, nbytes)),
+                                           dtype=torch.uint8)
+                    outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(nranks)]
+                    dist.all_gather(outs, src, group=group)
+                    allb = b"".join(bytes(o.numpy().tobytes()) for o in outs)
+                    ctypes.memmove(recv, allb, len(allb))
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported as a failed setup by the library
+                    return 1
+
+            self._cb = _HostAllgather(_allgather)
+            _check(_lib.ldu_comm_init_host(rank, nranks, device, ctypes.cast(self._cb, _P), None,
+                                           ctypes.byref(h)))
+        else:
+            if len(unique_id) != 128:
+                raise ValueError("unique id must be 128 bytes")
+            self._id = ctypes.create_string_buffer(unique_id, 128)
+            _check(_lib.ldu_comm_init(rank, nranks, self._id, device, ctypes.byref(h)))
         self.handle = h
         self.rank, self.nranks, self.device = rank, nranks, device
+
+    @classmethod
+    def host(cls, rank: int, nranks: int, device: int, group=None) -> "Comm":
+        """Peer-memory-only communicator bootstrapped over torch.distributed (gloo) ``group``."""
+        return cls(rank, nranks, None, device, _host_group=group)
 
     @staticmethod
     def unique_id() -> bytes:

@@ -35,16 +35,28 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile each translation unit in parallel (nvcc -c), then link the shared library."""
     if not force and not stale():
         return LIB
     nccl = nccl_root()
-    cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-           "-Xcompiler", "-fPIC", "-shared", "--extended-lambda", "-Xptxas", "-v" if verbose else "-O3",
-           "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nccl, "include"),
-           "-o", LIB + ".tmp", *SRCS,
-           "-L" + os.path.join(nccl, "lib"), "-l:libnccl.so.2",
-           "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
-    subprocess.check_call(cmd)
+    common = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
+              "-lineinfo", "-Xcompiler", "-fPIC", "--extended-lambda", "-Xptxas",
+              "-v" if verbose else "-O3", "-I" + os.path.join(ROOT, "include"),
+              "-I" + os.path.join(nccl, "include")]
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    objs, procs = [], []
+    for src in SRCS:
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        procs.append(subprocess.Popen(common + ["-c", src, "-o", obj]))
+    codes = [p.wait() for p in procs]
+    if any(codes):
+        raise subprocess.CalledProcessError(max(codes), "nvcc -c")
+    subprocess.check_call(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+                           "-o", LIB + ".tmp", *objs,
+                           "-L" + os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+                           "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")])
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

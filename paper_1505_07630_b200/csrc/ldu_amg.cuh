@@ -87,6 +87,13 @@ enum { PREC_AMG = 0, PREC_DIC = 1 };
 // largest level of its lower neighbours, so every cell of a level depends only on earlier levels
 // in the forward sweep and on later levels in the backward sweep), with each cell's strictly-lower
 // and strictly-upper couplings stored row by row in that order.
+// ELL width of the DIC sweep rows: the widths k_dic_ell is instantiated for (1-4, 6, 8); rows
+// wider than 8 keep CSR (returns 0).  Shared by the setup and the launch dispatch.
+inline int dic_ell_width(int W) {
+  if (W <= 0 || W > 8) return 0;
+  return W <= 4 ? W : (W <= 6 ? 6 : 8);
+}
+
 struct DicFactor {
   int nLev = 0;
   std::vector<int> levPtr;       // host [nLev + 1] positions in perm

@@ -1420,18 +1420,22 @@ void dic_setup(ldu_handle h) {
     lp[nPad] = (int)ol;
     up[nPad] = (int)ou;
     // ELL copies (position-major) when the rows are short
+    // host staging of the ELL copies lives until the final stream synchronisation below (the
+    // uploads are stream-ordered on s like every other upload of this setup)
+    std::vector<int> ecLo, ecUp;
+    std::vector<double> evLo, evUp;
     auto ell = [&](const std::vector<int>& P, const std::vector<int>& C, const std::vector<double>& V,
-                   int& w, int*& dc, double*& dv) {
-      int W = 0;
-      for (int k = 0; k < nPad; ++k) W = std::max(W, P[k + 1] - P[k]);
-      if (W == 0 || W > 8) {
-        w = W;
+                   int& w, int*& dc, double*& dv, std::vector<int>& ec, std::vector<double>& ev) {
+      int Wmax = 0;
+      for (int k = 0; k < nPad; ++k) Wmax = std::max(Wmax, P[k + 1] - P[k]);
+      const int W = dic_ell_width(Wmax);
+      if (W == 0) {  // no rows, or rows wider than any ELL instantiation: CSR sweeps
+        w = Wmax;
         return;
       }
-      W = W <= 4 ? W : (W <= 6 ? 6 : 8);  // the widths the sweep kernels are instantiated for
       w = W;
-      std::vector<int> ec((size_t)W * nPad, -1);
-      std::vector<double> ev((size_t)W * nPad, 0.0);
+      ec.assign((size_t)W * nPad, -1);
+      ev.assign((size_t)W * nPad, 0.0);
       for (int k = 0; k < nPad; ++k)
         for (int j = P[k]; j < P[k + 1]; ++j) {
           ec[(size_t)(j - P[k]) * nPad + k] = C[j];
@@ -1439,13 +1443,14 @@ void dic_setup(ldu_handle h) {
         }
       dc = dmalloc<int>((size_t)W * nPad);
       dv = dmalloc<double>((size_t)W * nPad);
-      CUDA_CHECK(cudaMemcpy(dc, ec.data(), sizeof(int) * ec.size(), cudaMemcpyHostToDevice));
-      CUDA_CHECK(cudaMemcpy(dv, ev.data(), sizeof(double) * ev.size(), cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpyAsync(dc, ec.data(), sizeof(int) * ec.size(), cudaMemcpyHostToDevice, s));
+      CUDA_CHECK(cudaMemcpyAsync(dv, ev.data(), sizeof(double) * ev.size(), cudaMemcpyHostToDevice, s));
     };
     D.dLevPtr = dmalloc<int>(nLev + 1);
-    CUDA_CHECK(cudaMemcpy(D.dLevPtr, D.levPtr.data(), sizeof(int) * (nLev + 1), cudaMemcpyHostToDevice));
-    ell(lp, lc, lvv, D.wLo, D.eLoCol, D.eLoVal);
-    ell(up, uc, uvv, D.wUp, D.eUpCol, D.eUpVal);
+    CUDA_CHECK(cudaMemcpyAsync(D.dLevPtr, D.levPtr.data(), sizeof(int) * (nLev + 1),
+                               cudaMemcpyHostToDevice, s));
+    ell(lp, lc, lvv, D.wLo, D.eLoCol, D.eLoVal, ecLo, evLo);
+    ell(up, uc, uvv, D.wUp, D.eUpCol, D.eUpVal, ecUp, evUp);
     D.perm = dmalloc<int>(nPad);
     D.loPtr = dmalloc<int>(nPad + 1);
     D.loCol = dmalloc<int>(std::max(1LL, nnzL));

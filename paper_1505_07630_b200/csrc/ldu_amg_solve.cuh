@@ -611,13 +611,14 @@ void launch_dic_ell(int W, bool pdl, int b, int e, int nPad, const int* perm, co
 #define LDU_DIC_ELL(WW)                                                                         \
   launch_pdl(pdl, k_dic_ell<WW, FWD>, g, kBlock, s, b, e, nPad, perm, ecol, eval, rD, f, z, st); \
   return;
-  switch (W) {
+  switch (dic_ell_width(W)) {  // the setup stored exactly this width (same helper)
     case 1: LDU_DIC_ELL(1)
     case 2: LDU_DIC_ELL(2)
     case 3: LDU_DIC_ELL(3)
     case 4: LDU_DIC_ELL(4)
-    case 5: case 6: LDU_DIC_ELL(6)
-    default: LDU_DIC_ELL(8)
+    case 6: LDU_DIC_ELL(6)
+    case 8: LDU_DIC_ELL(8)
+    default: throw Error(LDU_ERR_STATE, "DIC ELL width " + std::to_string(W) + " has no sweep kernel");
   }
 #undef LDU_DIC_ELL
 }
@@ -787,10 +788,11 @@ void ensure_amg_work(ldu_handle h, bool pipelined) {
   }
 }
 
-// Multi-rank (block-Jacobi, reading Z33): the V-cycle is local; the SpMV exchanges the halo over
-// NCCL (amul_dev) and every reduction is an allgather of the local sums + the control kernel.
-// Pipelined: the allgather of iteration i's fused sums runs on the reduction stream while the
-// V-cycle m_i = B w_i and n_i = A m_i run (neither needs alpha_i, beta_i): P:97's overlap.
+// Multi-rank (block-Jacobi, reading Z33): the V-cycle is local; the SpMV exchanges the halo
+// (amul_dev) and every reduction is a cross-rank gather of the local sums + the control kernel,
+// both over the peer mailboxes by default (the reducing kernel's last block publishes its sums,
+// red_loop) or over NCCL (LDU_P2P=0).  Pipelined: the gather of iteration i's fused sums is
+// overlapped with the V-cycle m_i = B w_i and n_i = A m_i (neither needs alpha_i, beta_i): P:97.
 long long enqueue_amg_iters_mr(ldu_handle h, bool pipelined, int batch, cudaStream_t s,
                                bool profile) {
   AmgHierarchy* H = h->amg;
@@ -799,7 +801,7 @@ long long enqueue_amg_iters_mr(ldu_handle h, bool pipelined, int batch, cudaStre
   for (int it = 0; it < batch; ++it) {
     prof_mark(h, profile, 4 * it + 0, s);
     if (!pipelined) {
-      const Red rr = red_of(h, CTL_NONE, false, H->L ? H->gPost : h->grid);
+      const Red rr = red_loop(h, CTL_NONE, false, H->L ? H->gPost : h->grid);
       kernels += enqueue_vcycle(h, h->r, H->zk, s, h->st, &rr);
       prof_mark(h, profile, 4 * it + 1, s);
       allgather_ctl(h, CTL_AMG_RHO, 1, s, kernels);
@@ -807,18 +809,26 @@ long long enqueue_amg_iters_mr(ldu_handle h, bool pipelined, int batch, cudaStre
       k_amg_p<<<h->grid, kBlock, 0, s>>>(h->n, H->zk, h->p0, h->x, h->st);
       ++kernels;
       amul_dev(h, h->p0, h->q, s, kernels);
-      k_amg_dot<<<h->grid, kBlock, 0, s>>>(h->n, h->p0, h->q, h->st, red_of(h, CTL_NONE, false));
+      k_amg_dot<<<h->grid, kBlock, 0, s>>>(h->n, h->p0, h->q, h->st, red_loop(h, CTL_NONE, false));
       ++kernels;
       allgather_ctl(h, CTL_CG_A, 1, s, kernels);
-      k_amg_passB<<<h->grid, kBlock, 0, s>>>(h->n, h->q, h->r, h->st, red_of(h, CTL_NONE, false));
+      k_amg_passB<<<h->grid, kBlock, 0, s>>>(h->n, h->q, h->r, h->st, red_loop(h, CTL_NONE, false));
       ++kernels;
       allgather_ctl(h, CTL_AMG_B, 1, s, kernels);
+    } else if (h->p2pOn) {  // the sums published by the previous U (or the init) wait in the mailboxes
+      kernels += enqueue_vcycle(h, h->w, H->m, s, h->st, nullptr);
+      amul_dev(h, H->m, h->nv, s, kernels);
+      prof_mark(h, profile, 4 * it + 1, s);
+      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_PIPE_NEXT, h->st, h->p2pDesc, 0);
+      prof_mark(h, profile, 4 * it + 2, s);
+      k_amg_pipe_U<<<h->grid, kBlock, 0, s>>>(h->n, H->m, h->nv, h->z, H->qk, h->s, h->p0, h->x,
+                                              h->r, H->u, h->w, h->st, red_loop(h, CTL_NONE, false));
+      kernels += 2;
     } else {
       CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
       CUDA_CHECK(cudaStreamWaitEvent(h->red_stream, h->ev_fork, 0));
       NCCL_CHECK(ncclAllGather(h->sums, h->gsums, kMaxVals, ncclDouble, cm->red, h->red_stream));
       CUDA_CHECK(cudaEventRecord(h->ev_red, h->red_stream));
-      h->stats.allreduces++;
       kernels += enqueue_vcycle(h, h->w, H->m, s, h->st, nullptr);
       amul_dev(h, H->m, h->nv, s, kernels);
       prof_mark(h, profile, 4 * it + 1, s);
@@ -1003,20 +1013,20 @@ ldu_status amg_solve(ldu_handle h, int kind, bool pipelined, const double* b, do
     k_fill<<<small_grid(n), kBlock, 0, s>>>(n, 1.0, h->r);
     ++kernels;
     amul_dev(h, h->r, sumA, s, kernels);
-    k_sum_x<<<h->grid, kBlock, 0, s>>>(n, h->x, h->st, red_of(h, CTL_XBAR, !mr));
+    k_sum_x<<<h->grid, kBlock, 0, s>>>(n, h->x, h->st, red_loop(h, CTL_XBAR, !mr));
     ++kernels;
     if (mr) allgather_ctl(h, CTL_XBAR, 2, s, kernels);
   }
   amul_dev(h, h->x, Ax0, s, kernels);
   k_resid<<<h->grid, kBlock, 0, s>>>(n, bin, Ax0, sumA, h->rD, h->r, h->st,
-                                     red_of(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, !mr));
+                                     red_loop(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, !mr));
   ++kernels;
   if (mr) allgather_ctl(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, 3, s, kernels);
   if (pipelined) {  // u0 = B r0; w0 = A u0; first fused reduction
     kernels += enqueue_vcycle(h, h->r, H->u, s, h->st, nullptr);
     amul_dev(h, H->u, h->w, s, kernels);
     k_amg_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->r, H->u, h->w, h->st,
-                                               red_of(h, CTL_PIPE_TOP, !mr));
+                                               red_loop(h, CTL_PIPE_TOP, !mr));
     ++kernels;
     if (mr) {  // its allgather is issued by the first loop trip; k = -1 so that trip evaluates i = 0
       static const int minus_one = -1;
@@ -1052,7 +1062,6 @@ ldu_status amg_solve(ldu_handle h, int kind, bool pipelined, const double* b, do
   int batches = 0;
   // multi-rank pipelined needs one more trip: the decision on r_i is taken after trip i's allgather
   const long long trips = (long long)maxIter + ((pipelined && mr) ? 1 : 0);
-  const long long redPerIter = mr ? (pipelined ? 0 : 3) : 0;  // pipelined counted at enqueue
   if (maxIter > 0) {
     for (;;) {
       CUDA_CHECK(cudaGraphLaunch(H->graph[gi], s));
@@ -1094,7 +1103,8 @@ ldu_status amg_solve(ldu_handle h, int kind, bool pipelined, const double* b, do
   CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]));
   h->stats.iterMs = ms;
   h->stats.kernels = kernels + (long long)batches * H->graphKernels[gi];
-  h->stats.allreduces = mr ? (long long)batches * batch * (pipelined ? 1 : redPerIter) : 0;
+  h->stats.allreduces = mr ? (long long)sh->nRed : 0;  // counted on the device (run_ctl)
+  h->stats.reductions = sh->nRed;
   h->stats.iterations = sh->iter;
   if (profile)  // pass 0 = V-cycle, pass 1 = Krylov passes, over the iterations that did work
     for (long long g = (pipelined && mr) ? 1 : 0;

@@ -112,6 +112,24 @@ ldu_status ldu_comm_init(int rank, int nRanks, const void* id128, int cudaDevice
   });
 }
 
+ldu_status ldu_comm_init_host(int rank, int nRanks, int cudaDevice, ldu_host_allgather_fn fn,
+                              void* ctx, ldu_comm* out) {
+  return guard("ldu_comm_init_host", [&] {
+    if (!fn || !out) ldu::fail_arg("NULL argument");
+    if (nRanks < 1 || rank < 0 || rank >= nRanks) ldu::fail_arg("bad rank / nRanks");
+    if (nRanks > 64) ldu::fail_arg("the peer-memory path supports <= 64 ranks");
+    CUDA_CHECK(cudaSetDevice(cudaDevice));
+    ldu_comm c = new ldu_comm_s();
+    c->rank = rank;
+    c->nRanks = nRanks;
+    c->device = cudaDevice;
+    c->hostAllgather = fn;
+    c->hostCtx = ctx;
+    *out = c;
+    return LDU_OK;
+  });
+}
+
 ldu_status ldu_comm_destroy(ldu_comm c) {
   return guard("ldu_comm_destroy", [&] {
     if (!c) return LDU_OK;
@@ -148,7 +166,10 @@ ldu_status ldu_setup(int nCells, int nFaces, const int* lowerAddr, const int* up
       CUDA_CHECK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
       CUDA_CHECK(cudaStreamCreateWithFlags(&h->red_stream, cudaStreamNonBlocking));
       CUDA_CHECK(cudaStreamCreateWithFlags(&h->halo_stream, cudaStreamNonBlocking));
-      h->stream = h->own_stream;
+      // the caller's stream defaults to the legacy default stream (CUDA stream 0, where torch
+      // and plain cudaMemcpy work by default): every call orders its work after it and the
+      // caller's later work after the call, so device inputs written there are never raced
+      h->stream = cudaStreamLegacy;
       for (auto* e : {&h->ev[0], &h->ev[1], &h->ev[2], &h->ev[3]})
         CUDA_CHECK(cudaEventCreate(e));
       for (auto* e : {&h->ev_fork, &h->ev_red, &h->ev_halo, &h->ev_pack})
@@ -167,7 +188,7 @@ ldu_status ldu_setup(int nCells, int nFaces, const int* lowerAddr, const int* up
 ldu_status ldu_set_stream(ldu_handle h, void* cudaStream) {
   return guard("ldu_set_stream", [&] {
     if (!h) ldu::fail_arg("handle is NULL");
-    h->stream = cudaStream ? (cudaStream_t)cudaStream : h->own_stream;
+    h->stream = cudaStream ? (cudaStream_t)cudaStream : cudaStreamLegacy;
     return LDU_OK;
   });
 }

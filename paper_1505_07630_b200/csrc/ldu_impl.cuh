@@ -92,6 +92,7 @@ struct State {
   int status;        // ldu_status
   int xpending;      // classical: alpha * p_k not yet added to x
   int zero_x;        // ||b|| == 0 => x := 0
+  int nRed;          // reductions consumed by a control step this solve (device counter)
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -111,6 +112,11 @@ struct ldu_comm_s {
   int rank = 0, nRanks = 1, device = 0;
   ncclComm_t red = nullptr;   // reductions (allgather of fused partial sums)
   ncclComm_t halo = nullptr;  // halo send / recv
+  // host bootstrap (ldu_comm_init_host): no NCCL; setup exchanges through the caller's host
+  // all-gather, every in-solve exchange over the peer-memory mailboxes
+  ldu_host_allgather_fn hostAllgather = nullptr;
+  void* hostCtx = nullptr;
+  bool nccl() const { return red != nullptr; }
 };
 
 namespace ldu {
@@ -210,6 +216,7 @@ struct ldu_handle_s {
 namespace ldu {
 struct P2PDesc;
 void p2p_setup(ldu_handle h);
+void host_allgather(ldu_comm cm, const void* send, void* recv, size_t bytes);
 void p2p_release(ldu_handle h);
 // setup (ldu_setup.cu)
 void build_layout(ldu_handle h, const int* l, const int* u, const double* diag,

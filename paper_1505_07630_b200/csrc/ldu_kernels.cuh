@@ -277,6 +277,7 @@ enum Ctl : int { CTL_NONE = 0, CTL_CG_INIT, CTL_PIPE_SCALE, CTL_XBAR, CTL_CG_A, 
                  CTL_PIPE_TOP, CTL_PIPE_NEXT, CTL_AMG_RHO, CTL_AMG_B };
 
 __device__ __forceinline__ void run_ctl(int ctl, State* st, const double* s) {
+  if (ctl != CTL_NONE) st->nRed += 1;  // device-side reduction count (ldu_solve_stats)
   switch (ctl) {
     case CTL_CG_INIT: ctl_cg_init(st, s); break;
     case CTL_PIPE_SCALE: ctl_scale(st, s[0]); break;

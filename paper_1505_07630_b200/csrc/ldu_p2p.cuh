@@ -35,6 +35,12 @@ struct P2PDesc {
   int rank, nRanks, nIf;
   unsigned long long seqRed, seqHalo;   // last consumed sequence numbers (device state)
   unsigned long long seqHaloSend;       // last sent halo exchange (advanced only by the pack)
+  // Fused pipelined loop: (k, done) of the State as the fix-up of iteration i saw them.  The pack
+  // of exchange i+1 runs on the halo stream concurrently with the control step of iteration
+  // i+1, which advances k and may set done; the pack reads this snapshot instead of the live
+  // State, so its buffer choice and its send/skip decision match what the consumer side assumes
+  // (the control step retires an exchange exactly when the snapshot said it was sent).
+  int snapK, snapDone;
   char* base[kP2PMaxRanks];             // mailbox of every rank (own = local pointer)
   int ifNeighbor[kP2PMaxIf];            // peer rank of my interface k
   int ifLocalOff[kP2PMaxIf];            // my packed face offset of interface k

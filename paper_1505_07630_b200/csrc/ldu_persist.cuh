@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kBlock) k_pipe_persist(Fmt A, const double* __
     persist_sum<3>(part, ld, gridDim.x, sums);
     if (threadIdx.x == 0) {
       st.k += 1;
+      st.nRed += 1;
       ctl_pipe_top(&st, sums);
     }
     __syncthreads();
@@ -130,7 +131,10 @@ __global__ void __launch_bounds__(kBlock) k_cg_persist(Fmt A, const double* __re
       persist_store<1>(v, partA, ld);
       grid.sync();
       persist_sum<1>(partA, ld, gridDim.x, sums);
-      if (threadIdx.x == 0) ctl_cg_A(&st, sums);
+      if (threadIdx.x == 0) {
+        st.nRed += 1;
+        ctl_cg_A(&st, sums);
+      }
       __syncthreads();
       if (st.done) break;
     }
@@ -147,7 +151,10 @@ __global__ void __launch_bounds__(kBlock) k_cg_persist(Fmt A, const double* __re
       persist_store<2>(v, partB, ld);
       grid.sync();
       persist_sum<2>(partB, ld, gridDim.x, sums);
-      if (threadIdx.x == 0) ctl_cg_B(&st, sums);
+      if (threadIdx.x == 0) {
+        st.nRed += 1;
+        ctl_cg_B(&st, sums);
+      }
       __syncthreads();
     }
   }

@@ -216,7 +216,10 @@ struct TmpFree {
 void build_layout(ldu_handle h, const int* l_in, const int* u_in, const double* diag_in,
                   const double* lower_in, const double* upper_in, const ldu_interfaces* ifs) {
   const int n = h->n, nf = h->nf;
-  cudaStream_t s = h->stream;
+  cudaStream_t s = h->own_stream;
+  // device-pointer inputs may have been written on the caller's stream (legacy by default)
+  CUDA_CHECK(cudaEventRecord(h->ev_fork, h->stream));
+  CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_fork, 0));
   TmpFree tmp;
 
   int* l = nf ? tmp.add(to_device(l_in, nf, s)) : nullptr;

@@ -495,23 +495,28 @@ __global__ void __launch_bounds__(kBlock, MINB) k_pipe_SU(Fmt A, const double* _
 
 // Halo send fused with the pack: the operand at every interface face is stored straight into the
 // neighbour's mailbox over NVLink; the last block raises the neighbours' flags.
+// gateK / gateDone (NULL = ungated, k = 0): the iteration index that selects the ping-pong half
+// and the done flag that skips the send.  The fused pipelined loop passes the fix-up's snapshot
+// (P2PDesc::snapK / snapDone), never the live State the concurrent control step is updating.
 __global__ void __launch_bounds__(kBlock) k_pack_p2p(int nIfFaces, const int* __restrict__ fc,
                                                      const int* __restrict__ faceIf, int mode,
                                                      const double* a,
                                                      const double* __restrict__ rD,
                                                      const double* p0, const double* p1,
-                                                     const State* st, P2PDesc* d,
+                                                     const State* st, const int* gateK,
+                                                     const int* gateDone, P2PDesc* d,
                                                      unsigned* ticket) {
-  if (st->done) return;
+  if (gateDone && *gateDone) return;
+  const int k = gateK ? *gateK : 0;
   double beta = 0.0;
   const double* pold = nullptr;
-  if (mode == PACK_CG_P) {
+  if (mode == PACK_CG_P) {  // classical: forked and joined between two control steps (no race)
     beta = st->beta;
-    pold = (st->k & 1) ? p0 : p1;
+    pold = (k & 1) ? p0 : p1;
   }
   const unsigned long long seq = d->seqHaloSend + 1;
   const int par = (int)(seq & 1);
-  if (mode == PACK_SCALED_W) a = (st->k & 1) ? p0 : p1;  // w_{i+1} written by the fused pass i
+  if (mode == PACK_SCALED_W) a = (k & 1) ? p0 : p1;  // w_{i+1} written by the fused pass i
   GRID_STRIDE(i, nIfFaces) {
     const int c = fc[i];
     double v = a[c];
@@ -551,7 +556,7 @@ __global__ void k_iface_apply_p2p(int nIfCells, const int* __restrict__ cell,
                                   const int* __restrict__ ptr, const int* __restrict__ fidx,
                                   const double* __restrict__ coeff, double* __restrict__ y,
                                   const State* st, P2PDesc* d, int nIfFaces) {
-  if (st->done) return;
+  if (st && st->done) return;
   const double* recv = p2p_wait_halo(d, nIfFaces);
   GRID_STRIDE(i, nIfCells) {
     double corr = 0.0;
@@ -595,6 +600,10 @@ __global__ void __launch_bounds__(kBlock) k_pipe_fixup_p2p(int nIfCells, const i
                                                            double* w1, State* st, Red rd,
                                                            P2PDesc* d, int nIfFaces) {
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // snapshot for the pack of the next exchange
+    d->snapK = st->k;
+    d->snapDone = st->done;
+  }
   if (st->done) return;
   if (threadIdx.x == 0) tstamp(d, st->k, 4, 1);
   const double* recv = p2p_wait_halo(d, nIfFaces);
@@ -633,6 +642,12 @@ __global__ void k_ctl_p2p(int ctl, State* st, P2PDesc* d, int advanceHalo) {
   // init) will never be consumed once the solve ends here -- retire its sequence number so the
   // next solve cannot mistake its flag for a fresh one
   if (advanceHalo == 2 && st->done) d->seqHalo += 1;
+}
+
+// An ungated halo exchange (ldu_amul's, or amul_dev inside a solve) has been consumed by
+// k_iface_apply_p2p: retire its sequence number (one thread, after every block read the flags).
+__global__ void k_p2p_halo_consumed(P2PDesc* d) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) d->seqHalo += 1;
 }
 
 // multi-rank control: sum the allgathered per-rank sums in rank order, then run the step.
@@ -934,27 +949,46 @@ Red red_loop(ldu_handle h, int ctl, bool single, int grid = 0) {
 }
 
 // fork the NVLink halo send onto the halo stream (it overlaps the next bulk pass) / join it
-void p2p_pack(ldu_handle h, int mode, const double* a, cudaStream_t s);
-void p2p_pack_async(ldu_handle h, int mode, const double* a, cudaStream_t s) {
+enum Gate : int { GATE_NONE = 0, GATE_LIVE = 1, GATE_SNAP = 2 };
+void p2p_pack(ldu_handle h, int mode, const double* a, cudaStream_t s, int gate);
+void p2p_pack_async(ldu_handle h, int mode, const double* a, cudaStream_t s, int gate) {
   CUDA_CHECK(cudaEventRecord(h->ev_pack, s));
   CUDA_CHECK(cudaStreamWaitEvent(h->halo_stream, h->ev_pack, 0));
-  p2p_pack(h, mode, a, h->halo_stream);
+  p2p_pack(h, mode, a, h->halo_stream, gate);
   CUDA_CHECK(cudaEventRecord(h->ev_halo, h->halo_stream));
 }
 void p2p_join(ldu_handle h, cudaStream_t s) { CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_halo, 0)); }
 
-void p2p_pack(ldu_handle h, int mode, const double* a, cudaStream_t s) {
+// gate: GATE_SNAP (fused loop, PACK_SCALED_W) reads the fix-up's snapshot; GATE_LIVE (the
+// classical loop and the first exchange of the fused loop) reads the live State, which nothing
+// modifies concurrently there; GATE_NONE (amul_dev) always sends -- its consumer always reads.
+void p2p_pack(ldu_handle h, int mode, const double* a, cudaStream_t s, int gate) {
   const double* q0 = mode == PACK_SCALED_W ? h->w : h->p0;
   const double* q1 = mode == PACK_SCALED_W ? h->w2 : h->p1;
+  const int *gk = nullptr, *gd = nullptr;
+  if (gate == GATE_SNAP) {
+    gk = &h->p2pDesc->snapK;
+    gd = &h->p2pDesc->snapDone;
+  } else if (gate == GATE_LIVE) {
+    gk = &h->st->k;
+    gd = &h->st->done;
+  }
   k_pack_p2p<<<small_grid(h->nIfFaces), kBlock, 0, s>>>(
-      h->nIfFaces, h->ifFaceCells, h->ifFaceIf, mode, a, h->rD, q0, q1, h->st, h->p2pDesc,
-      h->ticket + 1);
+      h->nIfFaces, h->ifFaceCells, h->ifFaceIf, mode, a, h->rD, q0, q1, h->st, gk, gd,
+      h->p2pDesc, h->ticket + 1);
 }
 
 bool multi(ldu_handle h) { return h->comm && h->comm->nRanks > 1; }
 
-// allgather of the local sums and the control step (multi-rank only)
+// cross-rank reduction of the local sums + the control step (multi-rank only).  Peer-memory
+// path: the reducing kernel (launched with red_loop) has published its sums from its last
+// block; k_ctl_p2p gathers them in rank order.  NCCL path: allgather on the reduction stream.
 void allgather_ctl(ldu_handle h, int ctl, int nv, cudaStream_t s, long long& kernels) {
+  if (h->p2pOn) {
+    k_ctl_p2p<<<1, 32, 0, s>>>(ctl, h->st, h->p2pDesc, 0);
+    ++kernels;
+    return;
+  }
   ldu_comm cm = h->comm;
   CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
   CUDA_CHECK(cudaStreamWaitEvent(h->red_stream, h->ev_fork, 0));
@@ -963,7 +997,6 @@ void allgather_ctl(ldu_handle h, int ctl, int nv, cudaStream_t s, long long& ker
   CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_red, 0));
   k_ctl<<<1, 32, 0, s>>>(ctl, h->st, h->gsums, cm->nRanks, nv);
   ++kernels;
-  h->stats.allreduces++;
 }
 
 // halo exchange of the packed send buffer on the halo stream; returns after enqueueing.
@@ -988,6 +1021,18 @@ void wait_halo(ldu_handle h, cudaStream_t s) { CUDA_CHECK(cudaStreamWaitEvent(s,
 // y = A x including interfaces, all on stream s (x, y device, internal or user)
 void amul_dev(ldu_handle h, const double* x, double* y, cudaStream_t s, long long& kernels) {
   const bool haveIf = h->nIfFaces > 0;
+  if (haveIf && h->p2pOn) {  // ungated exchange over the peer mailboxes (both sides always run)
+    p2p_pack_async(h, PACK_PLAIN, x, s, GATE_NONE);
+    launch_amul(h, x, y, s);
+    p2p_join(h, s);
+    k_iface_apply_p2p<<<small_grid(h->nIfCells), kBlock, 0, s>>>(
+        h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx, h->ifCoeffs, y, nullptr, h->p2pDesc,
+        h->nIfFaces);
+    k_p2p_halo_consumed<<<1, 32, 0, s>>>(h->p2pDesc);
+    kernels += 4;
+    h->stats.haloBytes += 8LL * h->nIfFaces;
+    return;
+  }
   if (haveIf) {
     k_pack<<<small_grid(h->nIfFaces), kBlock, 0, s>>>(h->nIfFaces, h->ifFaceCells, PACK_PLAIN, x,
                                                       nullptr, nullptr, nullptr, nullptr, h->sendbuf);
@@ -1048,7 +1093,7 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
   if (mr && h->p2pOn) {  // halo and both reductions over NVLink peer memory, no NCCL kernels
     for (int it = 0; it < batch; ++it) {
       if (haveIf) {
-        p2p_pack_async(h, PACK_CG_P, h->r, s);
+        p2p_pack_async(h, PACK_CG_P, h->r, s, GATE_LIVE);
         ++kernels;
       }
       Red ra = red_loop(h, CTL_CG_A, false, h->gridA);
@@ -1153,7 +1198,7 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
                    ig, kBlock, s, h->nIfCells, (const int*)h->ifCell, (const int*)h->ifCellPtr,
                    (const int*)h->ifFaceIdx, (const double*)h->ifCoeffs, (const double*)h->rD,
                    (const double*)h->r, h->z, h->w, h->w2, h->st, ri, h->p2pDesc, h->nIfFaces);
-        p2p_pack_async(h, PACK_SCALED_W, nullptr, s);
+        p2p_pack_async(h, PACK_SCALED_W, nullptr, s, GATE_SNAP);
         kernels += 2;
       }
       trace_mark(h, it, 4, s);
@@ -1165,7 +1210,7 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
     const bool haveIf = h->nIfFaces > 0;
     for (int it = 0; it < batch; ++it) {
       if (haveIf) {
-        p2p_pack_async(h, PACK_SCALED, h->w, s);
+        p2p_pack_async(h, PACK_SCALED, h->w, s, GATE_LIVE);
         ++kernels;
       }
       prof_mark(h, profile, 4 * it + 0, s);
@@ -1217,7 +1262,6 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
       CUDA_CHECK(cudaStreamWaitEvent(h->red_stream, h->ev_fork, 0));
       NCCL_CHECK(ncclAllGather(h->sums, h->gsums, kMaxVals, ncclDouble, cm->red, h->red_stream));
       CUDA_CHECK(cudaEventRecord(h->ev_red, h->red_stream));
-      h->stats.allreduces++;
     }
     if (haveIf) {
       k_pack<<<small_grid(h->nIfFaces), kBlock, 0, s>>>(h->nIfFaces, h->ifFaceCells, PACK_SCALED,
@@ -1466,16 +1510,32 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     k_fill<<<small_grid(n), kBlock, 0, s>>>(n, 1.0, h->r);
     ++kernels;
     amul_dev(h, h->r, sumA, s, kernels);  // sumA = A 1 incl. interfaces
-    k_sum_x<<<h->grid, kBlock, 0, s>>>(n, h->x, h->st, red_of(h, CTL_XBAR, !mr));
+    k_sum_x<<<h->grid, kBlock, 0, s>>>(n, h->x, h->st, red_loop(h, CTL_XBAR, !mr));
     ++kernels;
     if (mr) allgather_ctl(h, CTL_XBAR, 2, s, kernels);
   }
   amul_dev(h, h->x, h->ybuf, s, kernels);
   k_resid<<<h->grid, kBlock, 0, s>>>(n, bin, h->ybuf, sumA, h->rD, h->r, h->st,
-                                     red_of(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, !mr));
+                                     red_loop(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, !mr));
   ++kernels;
   if (mr) allgather_ctl(h, pipelined ? CTL_PIPE_SCALE : CTL_CG_INIT, 3, s, kernels);
-  if (pipelined) {
+  if (pipelined && h->p2pOn && h->nIfFaces) {  // w0 = A (rD.r0) over the peer mailboxes
+    p2p_pack_async(h, PACK_SCALED, h->r, s, GATE_NONE);
+    launch_spmv_scaled(h, h->r, h->w, s);
+    p2p_join(h, s);
+    k_iface_apply_p2p<<<small_grid(h->nIfCells), kBlock, 0, s>>>(
+        h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx, h->ifCoeffs, h->w, nullptr,
+        h->p2pDesc, h->nIfFaces);
+    k_p2p_halo_consumed<<<1, 32, 0, s>>>(h->p2pDesc);
+    kernels += 4;
+    h->stats.haloBytes += 8LL * h->nIfFaces;
+    k_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->rD, h->r, h->w, h->st, red_loop(h, CTL_PIPE_TOP, !mr));
+    ++kernels;
+    if (h->fusePipe) {  // exchange 0 of the fused loop
+      p2p_pack(h, PACK_SCALED, h->w, s, GATE_LIVE);
+      ++kernels;
+    }
+  } else if (pipelined) {
     // w0 = A u0 with u0 = rD.r0 (incl. interfaces), then the first fused reduction
     if (h->nIfFaces) {
       k_pack<<<small_grid(h->nIfFaces), kBlock, 0, s>>>(h->nIfFaces, h->ifFaceCells, PACK_SCALED,
@@ -1495,7 +1555,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     k_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->rD, h->r, h->w, h->st, red_loop(h, CTL_PIPE_TOP, !mr));
     ++kernels;
     if (mr && h->p2pOn && h->fusePipe && h->nIfFaces) {  // exchange 0 of the fused loop
-      p2p_pack(h, PACK_SCALED, h->w, s);
+      p2p_pack(h, PACK_SCALED, h->w, s, GATE_LIVE);
       ++kernels;
     }
     // multi-rank: the allgather of these sums is issued by the first loop trip (overlapped)
@@ -1514,7 +1574,6 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     CUDA_CHECK(cudaEventRecord(h->ev[1], s));
     long long launches = 0;
     const int trips = tol == 0.0 ? std::max(1, maxIter) : std::max(1, std::min(maxIter, 256));
-    float persistMs = 0.f;
     if (maxIter > 0) {
       for (;;) {
         int ld = h->gridP, mt = trips;
@@ -1553,7 +1612,6 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
         if (sh->done || launches * (long long)trips > (long long)maxIter + 2) break;
       }
     }
-    (void)persistMs;
     CUDA_CHECK(cudaEventRecord(h->ev[2], s));
     h->stats.kernels = kernels + launches;
     // pending x update (classical) / x = 0 when b = 0, on the device: one host sync per solve
@@ -1574,6 +1632,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]));
     h->stats.iterMs = ms;
     h->stats.iterations = sh->iter;
+    h->stats.reductions = sh->nRed;
     if (profile) {  // no per-pass split inside the persistent kernel: whole iterations
       h->stats.passMs[pipelined ? 1 : 0] = ms;
       h->stats.passLaunches[pipelined ? 1 : 0] = sh->iter;
@@ -1623,7 +1682,6 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   }
   cudaGraphExec_t gexec = G.exec;
   const long long kpb = G.kernels;
-  const long long redPerIter = mr ? (pipelined ? 1 : 2) : 0;
   const long long haloPerIter = h->nIfFaces ? 8LL * h->nIfFaces : 0;
   long long launched = 0;
   int batches = 0;
@@ -1666,7 +1724,6 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     }
   }
   launched = (long long)batches * kpb;
-  h->stats.allreduces += (long long)batches * batch * redPerIter;
   h->stats.haloBytes += (long long)batches * batch * haloPerIter;
   CUDA_CHECK(cudaEventRecord(h->ev[2], s));
 
@@ -1738,6 +1795,8 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   }
   h->stats.kernels = kernels + launched;
   h->stats.iterations = sh->iter;
+  h->stats.reductions = sh->nRed;                      // counted on the device (run_ctl)
+  h->stats.allreduces = mr ? (long long)sh->nRed : 0;  // every multi-rank control step gathers
   if (profile) {  // passes that did work: trips 0 .. iter-1 (multi-rank pipelined: 1 .. iter)
     const long long first = (pipelined && mr) ? 1 : 0;
     for (long long g = first; g < first + sh->iter && g < (long long)passT.size() / 2; ++g)
@@ -1811,19 +1870,21 @@ void p2p_setup(ldu_handle h) {
   }
   char* dbuf = dmalloc<char>((size_t)R * (sizeof(cudaIpcMemHandle_t) + sizeof(int) * TW) + 64);
   char* dsend = dbuf;
-  char* drecv = dbuf + sizeof(cudaIpcMemHandle_t) + sizeof(int) * TW;
   const size_t rec = sizeof(cudaIpcMemHandle_t) + sizeof(int) * TW;
   std::vector<char> hsend(rec), hrecv(rec * R);
   std::memcpy(hsend.data(), &mine, sizeof(mine));
   std::memcpy(hsend.data() + sizeof(mine), tbl.data(), sizeof(int) * TW);
-  char* dall = dmalloc<char>(rec * R);
-  CUDA_CHECK(cudaMemcpy(dsend, hsend.data(), rec, cudaMemcpyHostToDevice));
-  NCCL_CHECK(ncclAllGather(dsend, dall, rec, ncclChar, cm->red, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  CUDA_CHECK(cudaMemcpy(hrecv.data(), dall, rec * R, cudaMemcpyDeviceToHost));
-  dfree(dall);
+  if (cm->nccl()) {
+    char* dall = dmalloc<char>(rec * R);
+    CUDA_CHECK(cudaMemcpy(dsend, hsend.data(), rec, cudaMemcpyHostToDevice));
+    NCCL_CHECK(ncclAllGather(dsend, dall, rec, ncclChar, cm->red, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    CUDA_CHECK(cudaMemcpy(hrecv.data(), dall, rec * R, cudaMemcpyDeviceToHost));
+    dfree(dall);
+  } else {
+    host_allgather(cm, hsend.data(), hrecv.data(), rec);
+  }
   dfree(dbuf);
-  (void)drecv;
 
   P2PDesc d{};
   d.rank = me;
@@ -1874,11 +1935,25 @@ void p2p_setup(ldu_handle h) {
   h->p2pDesc = dmalloc<P2PDesc>(1);
   CUDA_CHECK(cudaMemcpy(h->p2pDesc, &d, sizeof(d), cudaMemcpyHostToDevice));
   // every rank's mailbox is mapped before anyone writes into it
-  int* flag = dmalloc<int>(1);
-  NCCL_CHECK(ncclAllReduce(flag, flag, 1, ncclInt, ncclSum, cm->red, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  dfree(flag);
+  if (cm->nccl()) {
+    int* flag = dmalloc<int>(1);
+    NCCL_CHECK(ncclAllReduce(flag, flag, 1, ncclInt, ncclSum, cm->red, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    dfree(flag);
+  } else {
+    CUDA_CHECK(cudaDeviceSynchronize());
+    char one = 1;
+    std::vector<char> all(R);
+    host_allgather(cm, &one, all.data(), 1);  // barrier
+  }
   h->p2pOn = true;
+}
+
+// the caller's host all-gather of a host-bootstrapped comm (setup only, never inside a solve)
+void host_allgather(ldu_comm cm, const void* send, void* recv, size_t bytes) {
+  if (!cm->hostAllgather) throw Error(LDU_ERR_STATE, "comm has neither NCCL nor a host all-gather");
+  if (cm->hostAllgather(cm->hostCtx, send, recv, (unsigned long long)bytes) != 0)
+    throw Error(LDU_ERR_INVALID_ARG, "the host all-gather callback failed");
 }
 
 void p2p_release(ldu_handle h) {
@@ -2095,7 +2170,7 @@ void configure(ldu_handle h) {
   CUDA_CHECK(cudaMallocHost((void**)&h->st_host, sizeof(State)));
   if (h->comm && h->comm->nRanks > 1) {
     const char* v = std::getenv("LDU_P2P");
-    if (!v || std::atoi(v) != 0) p2p_setup(h);
+    if (!h->comm->nccl() || !v || std::atoi(v) != 0) p2p_setup(h);  // host comm: peer memory only
   }
 }
 

@@ -15,6 +15,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -24,16 +25,9 @@ import meshgen  # noqa: E402
 
 
 def main():
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from dist_boot import boot
+    rank, world, comm = boot()
     import paper_1505_07630_b200 as ldu
-
-    uid = [ldu.Comm.unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    comm = ldu.Comm(rank, world, uid[0], local)
     dic = len(sys.argv) > 1 and sys.argv[1] == "dic"
     cases = {
         "hex": lambda: meshgen.hex_laplacian(24, 20, 32, dirichlet=dict(x0=1.0)),

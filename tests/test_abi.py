@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_functions():
         assert name in exported, name
         assert name in ldu.SIGNATURES, name
-    assert ldu.abi_version() == 1
+    assert ldu.abi_version() == 2
 
 
 def test_library_is_sm100a():

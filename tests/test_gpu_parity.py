@@ -111,6 +111,9 @@ def test_solve_parity(ldu, case, solver, persist, monkeypatch):
     keep = ohist[:m] > 1e-6
     np.testing.assert_allclose(hist[:m][keep], ohist[:m][keep], rtol=1e-5)
     assert stats["iterations"] == it and stats["kernels"] > 0 and stats["allreduces"] == 0
+    # device-counted grid-wide reductions (reading Z4): the r0 reduction plus 2 per
+    # classical iteration; pipelined: r0, (gamma_0, delta_0, rr_0), then ONE per iteration
+    assert stats["reductions"] == (1 + 2 * it if solver == "pcg" else 2 + it), stats
 
 
 @pytest.mark.parametrize("persist", ["0", "1"])

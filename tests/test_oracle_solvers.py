@@ -235,6 +235,31 @@ def test_openfoam_norm_factor():
     assert abs(np.abs(r).sum() / np.abs(b).sum() - res) < 1e-8 * max(res, 1e-12) + 1e-12
 
 
+@pytest.mark.parametrize("solver", ["pcg", "pipecg_j", "pipecg_l"])
+def test_openfoam_norm_factor_warm_start_golden(solver):
+    """Reading Z1 OpenFOAM normFactor with x0 != 0 against the hand-computed 3-cell example of
+    tests/golden/spec_examples.txt (of_norm_3cell): res0 = 7/11 exactly as printed there; both
+    xbar*sumA terms, the mean (not the sum) of x0 and the sign of r0 all enter it."""
+    ex = load_spec_examples()["of_norm_3cell"]
+    sys = meshgen.LduSystem(nCells=ex["n"], lowerAddr=ex["l"], upperAddr=ex["u"],
+                            diag=ex["diag"], upper=ex["upper"])
+    x0 = np.array([float(v) for v in ex["expected"]["x0"].split(",")])
+    res0 = float(ex["expected"]["res0"])
+    nf = float(ex["expected"]["normFactor"])
+    kw = dict(tol=1e-12, maxIter=50, norm=oracle.NORM_OPENFOAM, history=True)
+    if solver == "pcg":
+        st, x, it, res, h = oracle.pcg(sys, ex["vec"], x0=x0, **kw)
+    else:
+        mode = oracle.JACOBI if solver == "pipecg_j" else oracle.LITERAL
+        st, x, it, res, h = oracle.pipecg(sys, ex["vec"], x0=x0, mode=mode, **kw)
+    assert st == oracle.OK
+    assert abs(h[0] - res0) <= 1e-15
+    # the final criterion is sum|b - A x| / normFactor, normFactor fixed at the x0 value (11)
+    r = ex["vec"] - sys.dense() @ x
+    assert abs(np.abs(r).sum() / nf - res) <= 1e-10
+    assert it <= 3  # n = 3: exact termination in <= n steps
+
+
 @pytest.mark.slow
 def test_table2_iteration_ratio():
     """Table 2: absolute counts are unpinned (RHS/criterion unknown), but the
