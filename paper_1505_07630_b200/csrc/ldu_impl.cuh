@@ -210,6 +210,14 @@ struct ldu_handle_s {
   std::vector<char*> peerMailbox;        // IPC-mapped mailboxes of the other ranks
   ldu::P2PDesc* p2pDesc = nullptr;       // device descriptor
   int* ifFaceIf = nullptr;               // [nIfFaces] interface index of each packed face
+  // multi-rank fused pipelined pass (k_pipe_SU_mr): rows are visited in the rotated order
+  // c = (mrGapStart + t) mod n so the largest interface-free run of rows (t < mrGapLen) comes
+  // first and the rows that need the halo come last; mrTailIf[t - mrGapLen] = interface-cell
+  // index of position t (or -1)
+  int mrGapStart = 0, mrGapLen = 0;
+  int* mrTailIf = nullptr;
+  int gridSUmr = 0, mrPre = 4;           // grid / pre-phase rows per thread (LDU_MR_PRE: 0, 4, 8)
+  bool mrFuse = true;                    // one kernel per iteration (LDU_MR_FUSE=0: pack + fix-up)
   unsigned long long* tbuf = nullptr;    // LDU_TRACE device timestamps
 };
 

@@ -26,8 +26,14 @@ struct MailboxLayout {
   static constexpr size_t redFlag = 0;
   static constexpr size_t haloFlag = redFlag + sizeof(uint64_t) * 2 * kP2PMaxRanks;
   static constexpr size_t red = haloFlag + sizeof(uint64_t) * 2 * kP2PMaxIf;
-  static constexpr size_t recv = red + sizeof(double) * 2 * kP2PMaxRanks * 4;
-  static size_t bytes(int nIfFaces) { return recv + sizeof(double) * 2 * (size_t)nIfFaces; }
+  // low-latency (LL) slots of the one-kernel pipelined loop: every 8-byte word carries 32 bits
+  // of payload and the 32-bit sequence number of its message, so a reader that sees the
+  // expected sequence number in a word has its payload -- no fence, no separate flag.
+  // redLL: [parity][source rank][4 values][2 words]; haloLL: [parity][face][2 words]
+  static constexpr size_t redLL = red + sizeof(double) * 2 * kP2PMaxRanks * 4;
+  static constexpr size_t recv = redLL + sizeof(uint64_t) * 2 * kP2PMaxRanks * 4 * 2;
+  __host__ __device__ static size_t haloLL(int nIfFaces) { return recv + sizeof(double) * 2 * (size_t)nIfFaces; }
+  __host__ __device__ static size_t bytes(int nIfFaces) { return haloLL(nIfFaces) + sizeof(uint64_t) * 2 * 2 * (size_t)nIfFaces; }
 };
 
 // Device-resident descriptor (one per handle).
@@ -77,6 +83,41 @@ __device__ __forceinline__ double* mb_red(char* b, int par, int src) {
 }
 __device__ __forceinline__ double* mb_recv(char* b, int par, int nIfFaces) {
   return reinterpret_cast<double*>(b + MailboxLayout::recv) + (size_t)par * nIfFaces;
+}
+
+// LL slots of the mailbox `b` (whose owner has nIfFaces packed interface faces)
+__device__ __forceinline__ uint64_t* mb_redll(char* b, int par, int src) {
+  return reinterpret_cast<uint64_t*>(b + MailboxLayout::redLL) + (size_t)(par * kP2PMaxRanks + src) * 8;
+}
+__device__ __forceinline__ uint64_t* mb_haloll(char* b, int par, int nIfFaces) {
+  return reinterpret_cast<uint64_t*>(b + MailboxLayout::haloLL(nIfFaces)) + (size_t)par * nIfFaces * 2;
+}
+
+// One fp64 value as two LL words (NCCL's LL protocol): each aligned 8-byte word is single-copy
+// atomic, so a reader that sees `flag` in both words holds both halves of this message's value.
+__device__ __forceinline__ void ll_store(uint64_t* p, double v, uint32_t flag) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long f = (unsigned long long)flag << 32;
+  const unsigned long long w0 = f | (bits & 0xffffffffull), w1 = f | (bits >> 32);
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+__device__ __forceinline__ bool ll_try(const uint64_t* p, uint32_t flag, double& v) {
+  unsigned long long w0, w1;
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+  if ((uint32_t)(w0 >> 32) != flag || (uint32_t)(w1 >> 32) != flag) return false;
+  v = __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+  return true;
+}
+// Bounded spin (~4 s at 2 GHz), as spin_until_geq.
+__device__ __forceinline__ double ll_load(const uint64_t* p, uint32_t flag) {
+  double v;
+  if (ll_try(p, flag, v)) return v;
+  const long long t0 = clock64();
+  while (!ll_try(p, flag, v)) {
+    if (clock64() - t0 > 8000000000LL) __trap();
+    __nanosleep(32);
+  }
+  return v;
 }
 
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {

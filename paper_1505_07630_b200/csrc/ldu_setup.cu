@@ -418,6 +418,33 @@ void build_layout(ldu_handle h, const int* l_in, const int* u_in, const double* 
     h->sendbuf = dmalloc<double>(h->nIfFaces);
     h->recvbuf = dmalloc<double>(h->nIfFaces);
     h->matrixBytes += 12LL * h->nIfFaces;
+    // rotation of the multi-rank fused pipelined pass: start right after the interface cell
+    // that opens the largest (cyclic) run of interface-free rows, so the rows needing the halo
+    // are visited last (z-slabs: the bulk of the slab first, then its two boundary planes)
+    {
+      const int m = (int)cells.size();
+      long long bestLen = -1;
+      int bestStart = 0;
+      for (int j = 0; j < m; ++j) {
+        const long long nxt = (j + 1 < m) ? cells[j + 1] : (long long)cells[0] + n;
+        const long long len = nxt - cells[j] - 1;
+        if (len > bestLen) {
+          bestLen = len;
+          bestStart = (cells[j] + 1) % n;
+        }
+      }
+      h->mrGapStart = bestStart;
+      h->mrGapLen = (int)std::min<long long>(bestLen, n - bestStart);  // the bulk never wraps
+      const int tail = n - h->mrGapLen;
+      std::vector<int> tailIf(std::max(1, tail), -1);
+      for (int j = 0; j < m; ++j) {
+        long long t = (long long)cells[j] - bestStart;
+        if (t < 0) t += n;
+        if (t < h->mrGapLen || t >= n) throw Error(LDU_ERR_STATE, "internal: interface cell inside the gap");
+        tailIf[t - h->mrGapLen] = j;
+      }
+      h->mrTailIf = to_device(tailIf.data(), tailIf.size(), s);
+    }
   } else if (ifs && ifs->comm) {
     h->comm = ifs->comm;
     h->nRanks = ifs->comm->nRanks;

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kBlock) k_iface_cg(int nIfCells, const int* __
   finish_reduction<1>(v, rd, st);
 }
 
-enum Pack : int { PACK_PLAIN = 0, PACK_SCALED = 1, PACK_CG_P = 2, PACK_SCALED_W = 3 };
+enum Pack : int { PACK_PLAIN = 0, PACK_SCALED = 1, PACK_CG_P = 2, PACK_SCALED_W = 3, PACK_SCALED_LL = 4 };
 
 // Halo send buffer: the SpMV operand at the interface cells.
 __global__ void k_pack(int nIfFaces, const int* __restrict__ fc, int mode,
@@ -517,14 +517,20 @@ __global__ void __launch_bounds__(kBlock) k_pack_p2p(int nIfFaces, const int* __
   const unsigned long long seq = d->seqHaloSend + 1;
   const int par = (int)(seq & 1);
   if (mode == PACK_SCALED_W) a = (k & 1) ? p0 : p1;  // w_{i+1} written by the fused pass i
+  const bool ll = mode == PACK_SCALED_LL;
   GRID_STRIDE(i, nIfFaces) {
     const int c = fc[i];
     double v = a[c];
-    if (mode == PACK_SCALED || mode == PACK_SCALED_W) v = rD[c] * v;
+    if (mode == PACK_SCALED || mode == PACK_SCALED_W || ll) v = rD[c] * v;
     else if (mode == PACK_CG_P) v = fma(beta, pold[c], rD[c] * v);
-    const int k = faceIf[i];
-    double* dst = mb_recv(d->base[d->ifNeighbor[k]], par, d->ifRemoteTotal[k]);
-    dst[d->ifRemoteOff[k] + (i - d->ifLocalOff[k])] = v;
+    const int kk = faceIf[i];
+    if (ll) {  // exchange 0 of the one-kernel loop: LL words, no flag (the flag release is skipped)
+      uint64_t* dst = mb_haloll(d->base[d->ifNeighbor[kk]], par, d->ifRemoteTotal[kk]);
+      ll_store(dst + 2 * (size_t)(d->ifRemoteOff[kk] + (i - d->ifLocalOff[kk])), v, (uint32_t)seq);
+    } else {
+      double* dst = mb_recv(d->base[d->ifNeighbor[kk]], par, d->ifRemoteTotal[kk]);
+      dst[d->ifRemoteOff[kk] + (i - d->ifLocalOff[kk])] = v;
+    }
   }
   // one cumulative system-scope fence per block (after the barrier) orders the whole block's
   // remote stores before its ticket; the last block then releases the flags
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(kBlock) k_pack_p2p(int nIfFaces, const int* __
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
-    p2p_release_halo(d, seq);
+    if (!ll) p2p_release_halo(d, seq);
     d->seqHaloSend = seq;
     *ticket = 0u;
   }
@@ -623,6 +629,257 @@ __global__ void __launch_bounds__(kBlock) k_pipe_fixup_p2p(int nIfCells, const i
   if (threadIdx.x == 0) tstamp(d, st->k, 6, 2);
   finish_reduction<3>(v, rd, st);  // last block publishes the iteration's single reduction
   if (threadIdx.x == 0) tstamp(d, st->k, 7, 2);
+}
+
+// ---- multi-rank pipelined CG, ONE kernel per iteration -------------------------------------
+// ("only one collective communication per loop body ... overlapped by the sparse
+// matrix-vector multiplication kernel"; "single reduction followed by matrix-vector
+// multiplication".)  Iteration i = control step k_ctl_ll (gathers the single reduction of i-1
+// from this rank's mailbox, alpha_i / beta_i) + k_pipe_SU_mr over all rows:
+//   * pre-phase, BEFORE griddepcontrol.wait: launched programmatically while the control step
+//     runs, every thread computes the internal SpMV n = A (rD w_i) of its first R rows
+//     (interface-free rows) into shared memory;
+//   * rows are visited in the rotated order c = (gapStart + t) mod n: the interface-free rows
+//     (t < gapLen) stream first, the rows next to a processor boundary come last, where the
+//     halo of exchange i (rD w_i at the neighbours' interface cells, written by the neighbours'
+//     pass i-1) has long arrived, so n_c includes the interface term exactly;
+//   * at interface cells the halo of exchange i+1 (rD w_{i+1}) is stored straight into the
+//     neighbours' mailboxes over NVLink;
+//   * the last block sums the partials in fixed order and stores (gamma, delta, rr) into every
+//     rank's mailbox, leaving the iteration index for the next pre-phase (snapK).
+// Halo values and sums travel as LL words (32-bit payload + 32-bit sequence number per 8-byte
+// word, NCCL's LL protocol): readers spin until the words carry the expected sequence number,
+// so the loop has no memory fence and no flag.  No pack, fix-up or halo stream: one HBM pass
+// and one kernel boundary per iteration.  MINB = 5 (48 registers): at 6 the accumulators spill
+// inside the streaming loop.
+struct MrTail {
+  int gapStart, gapLen;
+  const int* __restrict__ tailIf;   // [n - gapLen] interface-cell index of position t, or -1
+  const int* __restrict__ cellPtr;  // [nIfCells + 1] into faceIdx
+  const int* __restrict__ faceIdx;  // packed face index (interface order, then face order)
+  const double* __restrict__ coeff; // [nIfFaces] interfaceBouCoeffs
+  const int* __restrict__ faceIf;   // [nIfFaces] interface of each packed face
+  int nIfFaces;
+};
+
+// one row of the GV recurrences (shared by the bulk and the boundary loops of k_pipe_SU_mr)
+struct PipeRow {
+  double a, b;
+  bool l2;
+  __device__ __forceinline__ double apply(int c, double wc0, double nc, const double* __restrict__ rD,
+                                          double* __restrict__ z, double* __restrict__ s,
+                                          double* __restrict__ p, double* __restrict__ x,
+                                          double* __restrict__ r, double* __restrict__ wn,
+                                          double (&v)[3], double& rdc) const {
+    rdc = __ldg(rD + c);
+    const double rc0 = r[c];
+    const double zc = fma(b, z[c], nc);
+    const double sc = fma(b, s[c], wc0);
+    const double pc = fma(b, p[c], rdc * rc0);
+    z[c] = zc;
+    s[c] = sc;
+    p[c] = pc;
+    x[c] = fma(a, pc, x[c]);
+    const double rc = fma(-a, sc, rc0);
+    const double wc = fma(-a, zc, wc0);
+    r[c] = rc;
+    wn[c] = wc;
+    const double u = rdc * rc;
+    v[0] = fma(rc, u, v[0]);
+    v[1] = fma(wc, u, v[1]);
+    v[2] += l2 ? rc * rc : fabs(rc);
+    return wc;
+  }
+};
+
+// Boundary row (position t >= gapLen): interface term from the halo of exchange i (LL words,
+// sequence number flagIn), the recurrences, and the halo of exchange i+1 (rD w_{i+1}) as LL
+// words straight into the neighbours' mailboxes over NVLink (no fence, no flag).
+template <class Fmt>
+__device__ __forceinline__ void mr_boundary_row(const Fmt& A, int c, int ic, const double* __restrict__ rD,
+                                                const double* __restrict__ w, double* __restrict__ wn,
+                                                double* __restrict__ z, double* __restrict__ s,
+                                                double* __restrict__ p, double* __restrict__ x,
+                                                double* __restrict__ r, const PipeRow& P,
+                                                const MrTail& T, const P2PDesc* d,
+                                                const uint64_t* recv, uint32_t flagIn, int parOut,
+                                                uint32_t flagOut, double (&v)[3]) {
+  const double wc0 = __ldg(w + c);
+  double nc = row_apply(A, c, wc0, [&](int q) { return __ldg(rD + q) * __ldg(w + q); });
+  if (ic >= 0) {  // interface term of n = A (rD w): y[c] -= coeff * (rD w)_neighbour (Z10, Z23)
+    double corr = 0.0;
+    for (int f = __ldg(T.cellPtr + ic); f < __ldg(T.cellPtr + ic + 1); ++f) {
+      const int fi = __ldg(T.faceIdx + f);
+      corr = fma(__ldg(T.coeff + fi), ll_load(recv + 2 * (size_t)fi, flagIn), corr);
+    }
+    nc -= corr;
+  }
+  double rdc;
+  const double wc = P.apply(c, wc0, nc, rD, z, s, p, x, r, wn, v, rdc);
+  if (ic < 0) return;
+  const double hv = rdc * wc;
+  for (int f = __ldg(T.cellPtr + ic); f < __ldg(T.cellPtr + ic + 1); ++f) {
+    const int fi = __ldg(T.faceIdx + f);
+    const int kk = __ldg(T.faceIf + fi);
+    uint64_t* dst = mb_haloll(d->base[d->ifNeighbor[kk]], parOut, d->ifRemoteTotal[kk]);
+    ll_store(dst + 2 * (size_t)(d->ifRemoteOff[kk] + (fi - d->ifLocalOff[kk])), hv, flagOut);
+  }
+}
+
+template <class Fmt, int R, int MINB = 5>
+__global__ void __launch_bounds__(kBlock, MINB) k_pipe_SU_mr(Fmt A, const double* __restrict__ rD,
+                                                       double* w0, double* w1,
+                                                       double* __restrict__ z,
+                                                       double* __restrict__ s,
+                                                       double* __restrict__ p,
+                                                       double* __restrict__ x,
+                                                       double* __restrict__ r, State* st, Red rd,
+                                                       MrTail T, P2PDesc* d) {
+  __shared__ double preN[R > 0 ? R : 1][kBlock], preW[R > 0 ? R : 1][kBlock];
+  const int n = A.n;
+  const int stride = gridDim.x * kBlock;
+  const int base0 = blockIdx.x * kBlock;
+  const int tid = threadIdx.x;
+  const int gap = T.gapLen;
+  // ---- pre-phase (may run while the control step of this iteration is still waiting) ----
+  const int kpre = d->snapK + 1;  // left by the previous pass (or the init): this iteration
+  if (R > 0) {
+    const double* __restrict__ w = (kpre & 1) ? w1 : w0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int t = base0 + j * stride + tid;
+      if (t < gap) {
+        int c = T.gapStart + t;
+        if (c >= n) c -= n;
+        const double wc = __ldg(w + c);
+        preW[j][tid] = wc;
+        preN[j][tid] = row_apply(A, c, wc, [&](int q) { return __ldg(rD + q) * __ldg(w + q); });
+      }
+    }
+  }
+  pdl_wait();  // the control step has finished: alpha_i, beta_i, done
+  if (st->done) return;
+  const int k = st->k;
+  if (tid == 0) tstamp(d, k, 2, 1);
+  const PipeRow P{st->pa, st->pb, st->norm == LDU_NORM_L2};
+  const double* __restrict__ w = (k & 1) ? w1 : w0;
+  double* __restrict__ wn = (k & 1) ? w0 : w1;
+  double v[3] = {0.0, 0.0, 0.0};
+  const unsigned long long seqIn = d->seqHalo + 1, seqOut = d->seqHaloSend + 1;
+  auto boundary = [&]() {  // positions t >= gap, at most one block-row per block
+  {
+    int bb = base0;  // first block-row of this block that reaches past the gap
+    if (bb + kBlock <= gap) bb += ((gap - bb - kBlock) / stride + 1) * stride;
+    if (bb < n) {
+      if (tid == 0) tstamp(d, k, 4, 1);
+      const uint64_t* recv = mb_haloll(d->base[d->rank], (int)(seqIn & 1), T.nIfFaces);
+      for (int t = bb + tid; t < n; t += stride) {
+        if (t < gap) continue;
+        int c = T.gapStart + t;
+        if (c >= n) c -= n;
+        const int ic = __ldg(T.tailIf + (t - gap));
+        mr_boundary_row(A, c, ic, rD, w, wn, z, s, p, x, r, P, T, d, recv, (uint32_t)seqIn,
+                        (int)(seqOut & 1), (uint32_t)seqOut, v);
+      }
+      if (tid == 0) tstamp(d, k, 6, 2);
+    }
+  }
+  };
+  // ---- bulk: interface-free rows (positions t < gap) ----
+  {
+    int j = 0;
+    if (R > 0 && k == kpre) {
+#pragma unroll
+      for (; j < R; ++j) {
+        const int t = base0 + j * stride + tid;
+        if (t < gap) {
+          int c = T.gapStart + t;
+          if (c >= n) c -= n;
+          double rdc;
+          P.apply(c, preW[j][tid], preN[j][tid], rD, z, s, p, x, r, wn, v, rdc);
+        }
+      }
+    }
+    for (int t = base0 + j * stride + tid; t < gap; t += stride) {
+      const int c = T.gapStart + t;  // the gap never wraps (ldu_setup)
+      const double wc0 = __ldg(w + c);
+      const double nc = row_apply(A, c, wc0, [&](int q) { return __ldg(rD + q) * __ldg(w + q); });
+      double rdc;
+      P.apply(c, wc0, nc, rD, z, s, p, x, r, wn, v, rdc);
+    }
+  }
+  if (tid == 0) tstamp(d, k, 3, 2);
+  // ---- boundary rows last: the halo of exchange i has long arrived (measured: the order makes
+  // no difference, profiles/r02_multi) ----
+  boundary();
+  if (tid == 0) tstamp(d, k, 7, 2);
+  __shared__ double sm[3][32];
+  __shared__ bool last;
+  block_reduce<3>(v, sm);
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) rd.partials[q * rd.ld + blockIdx.x] = v[q];
+    __threadfence();
+    last = atomicAdd(rd.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  if (tid == 0) tstamp(d, k, 12, 0);
+  sum_partials<3>(rd.partials, rd.ld, gridDim.x, rd.sums, rd.ticket);
+  // the iteration's single reduction, as LL words, to every rank (lane q -> rank q)
+  const unsigned long long sq = d->seqRed + 1;
+  __syncthreads();
+  if (tid < d->nRanks) {
+    uint64_t* dst = mb_redll(d->base[tid], (int)(sq & 1), d->rank);
+    const double* sums = rd.sums;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) ll_store(dst + 2 * m, __ldcg(sums + m), (uint32_t)sq);
+  }
+  if (tid == 0) {
+    d->seqHaloSend = seqOut;
+    d->snapK = k;
+    tstamp(d, k, 13, 0);
+  }
+}
+
+// Control step of the one-kernel loop: gather iteration i-1's sums from the LL slots of this
+// rank's mailbox (lane q polls rank q), sum them in rank order, run CTL_PIPE_NEXT.  The first
+// trip (k = -1) gathers the init's reduction, published with the flag protocol.
+__global__ void k_ctl_ll(State* st, P2PDesc* d) {
+  pdl_wait();
+  pdl_trigger();  // the pass may launch now and run its pre-phase while we wait
+  if (st->done) return;
+  __shared__ double part[kP2PMaxRanks][3];
+  const int lane = threadIdx.x;
+  const unsigned long long sq = d->seqRed + 1;
+  if (st->k >= 0) {
+    char* me = d->base[d->rank];
+    for (int q = lane; q < d->nRanks; q += blockDim.x) {
+      const uint64_t* src = mb_redll(me, (int)(sq & 1), q);
+#pragma unroll
+      for (int m = 0; m < 3; ++m) part[q][m] = ll_load(src + 2 * m, (uint32_t)sq);
+    }
+  }
+  __syncthreads();
+  if (lane != 0) return;
+  tstamp(d, st->k + 1, 0, 0);
+  double sums[kMaxVals] = {0.0, 0.0, 0.0, 0.0};
+  if (st->k >= 0) {
+    for (int q = 0; q < d->nRanks; ++q)
+      for (int m = 0; m < 3; ++m) sums[m] += part[q][m];
+    d->seqRed = sq;
+  } else {
+    p2p_gather_sums<kMaxVals>(d, sums);
+  }
+  tstamp(d, st->k + 1, 1, 0);
+  if (d->nIf > 0 && st->k >= 0) d->seqHalo += 1;  // exchange i-1, consumed by pass i-1
+  run_ctl(CTL_PIPE_NEXT, st, sums);
+  if (d->nIf > 0 && st->done) d->seqHalo += 1;    // exchange i, sent by pass i-1, never read
+}
+
+// The fused multi-rank loop starts at k = -1 (its first control step evaluates i = 0).
+__global__ void k_mr_init(P2PDesc* d, const State* st) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) d->snapK = st->k;
 }
 
 // advanceHalo: 0 no halo exchange, 1 this step follows the consumption of one exchange,
@@ -1161,6 +1418,38 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
 long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profile) {
   long long kernels = 0;
   const bool mr = multi(h);
+  if (mr && h->p2pOn && h->fusePipe && h->mrFuse) {  // ONE kernel per iteration (k_pipe_SU_mr)
+    const bool haveIf = h->nIfFaces > 0;
+    MrTail T{h->mrGapStart, haveIf ? h->mrGapLen : h->n, h->mrTailIf, h->ifCellPtr, h->ifFaceIdx,
+             h->ifCoeffs, h->ifFaceIf, h->nIfFaces};
+    const bool pdl = h->pdl && h->trace.empty();
+    for (int it = 0; it < batch; ++it) {
+      trace_mark(h, it, 0, s);
+      launch_pdl(pdl && it > 0 && !profile, k_ctl_ll, 1, 64, s, h->st, h->p2pDesc);
+      ++kernels;
+      trace_mark(h, it, 1, s);
+      prof_mark(h, profile, 4 * it + 0, s);
+      prof_mark(h, profile, 4 * it + 1, s);
+      prof_mark(h, profile, 4 * it + 2, s);
+      Red ru = red_loop(h, CTL_NONE, false, h->gridSUmr);
+      with_format(h, [&](auto A) {
+        using Fmt = decltype(A);
+        auto go = [&](auto kern) {
+          launch_pdl(pdl && !profile, kern, h->gridSUmr, kBlock, s, A, (const double*)h->rD, h->w,
+                     h->w2, h->z, h->s, h->p0, h->x, h->r, h->st, ru, T, h->p2pDesc);
+        };
+        if (h->mrPre == 8) go(k_pipe_SU_mr<Fmt, 8>);
+        else if (h->mrPre == 4) go(k_pipe_SU_mr<Fmt, 4>);
+        else go(k_pipe_SU_mr<Fmt, 0>);
+      });
+      ++kernels;
+      prof_mark(h, profile, 4 * it + 3, s);
+      trace_mark(h, it, 2, s);
+      trace_mark(h, it, 3, s);
+      trace_mark(h, it, 4, s);
+    }
+    return kernels;
+  }
   if (mr && h->p2pOn && h->fusePipe) {  // fused S+U pass per iteration over peer memory
     // trip i: ctl_i (alpha_i, beta_i) -> k_pipe_SU over all rows (internal SpMV) -> [join the
     // halo stream] -> fix-up of the interface rows with exchange i (publishes the iteration's
@@ -1531,8 +1820,8 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     h->stats.haloBytes += 8LL * h->nIfFaces;
     k_pipe_dots<<<h->grid, kBlock, 0, s>>>(n, h->rD, h->r, h->w, h->st, red_loop(h, CTL_PIPE_TOP, !mr));
     ++kernels;
-    if (h->fusePipe) {  // exchange 0 of the fused loop
-      p2p_pack(h, PACK_SCALED, h->w, s, GATE_LIVE);
+    if (h->fusePipe) {  // exchange 0 of the fused loop (LL words for the one-kernel loop)
+      p2p_pack(h, h->mrFuse ? PACK_SCALED_LL : PACK_SCALED, h->w, s, GATE_LIVE);
       ++kernels;
     }
   } else if (pipelined) {
@@ -1565,6 +1854,10 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     // k = -1 so that CTL_PIPE_NEXT of the first iteration evaluates i = 0
     static const int minus_one = -1;
     CUDA_CHECK(cudaMemcpyAsync(&h->st->k, &minus_one, sizeof(int), cudaMemcpyHostToDevice, s));
+    if (h->p2pOn && h->fusePipe && h->mrFuse) {
+      k_mr_init<<<1, 32, 0, s>>>(h->p2pDesc, h->st);
+      ++kernels;
+    }
   }
   CUDA_CHECK(cudaEventRecord(h->ev[1], s));
 
@@ -1772,7 +2065,30 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
       acc[10] += (double)(a[10] - a[9]); // publish
       ++cnt;
     }
-    if (cnt)
+    if (cnt && h->mrFuse && h->fusePipe) {
+      double m[9] = {0};
+      int mc = 0;
+      for (int k = 5; k < std::min(sh->iter - 2, 250); ++k) {
+        unsigned long long a[16], nx0 = tb[(k + 1) * 16 + 0];
+        for (int q = 0; q < 16; ++q) a[q] = tb[k * 16 + q];
+        a[2] = ~a[2];
+        a[4] = ~a[4];
+        m[0] += (double)(a[1] - a[0]);    // ctl gather wait
+        m[1] += (double)(a[2] - a[1]);    // ctl end -> first block past pdl_wait
+        m[2] += (double)(a[3] - a[2]);    // -> last bulk end
+        m[3] += (double)(a[6] - a[4]);    // first boundary row begin -> last boundary end
+        m[4] += (double)(a[6] - a[2]);    // first block start -> last boundary end
+        m[5] += (double)(a[7] - a[3]);    // last bulk end -> last block at its ticket
+        m[6] += (double)(a[12] - a[7]);   // -> last block past the ticket
+        m[7] += (double)(a[13] - a[12]);  // sum + publish
+        m[8] += (double)(nx0 - a[13]);    // -> next ctl start
+        ++mc;
+      }
+      if (mc)
+        fprintf(stderr, "[ldu gtimer mr rank %d] us: ctlwait %.1f ->SU %.1f bulk %.1f boundary %.1f (from start %.1f) ->ticket %.1f ticket %.1f publish %.1f ->ctl %.1f\n",
+                h->rank, m[0] / mc / 1e3, m[1] / mc / 1e3, m[2] / mc / 1e3, m[3] / mc / 1e3, m[4] / mc / 1e3,
+                m[5] / mc / 1e3, m[6] / mc / 1e3, m[7] / mc / 1e3, m[8] / mc / 1e3);
+    } else if (cnt)
       fprintf(stderr, "[ldu gtimer rank %d] us: ctlwait %.1f ->SU %.1f SU %.1f ->fix %.1f fixwait %.1f fixwork %.1f fixfin %.1f (ticket %.1f sum %.1f publish %.1f) ->ctl %.1f\n",
               h->rank, acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3,
               acc[4] / cnt / 1e3, acc[5] / cnt / 1e3, acc[6] / cnt / 1e3, acc[8] / cnt / 1e3,
@@ -1983,8 +2299,12 @@ void configure(ldu_handle h) {
   // PDL on the multi-rank fused pipelined chain is opt-in: measured +0.7 % at 256^3 / 4 ranks,
   // but at 512^3 / 4 ranks it produced a wrong iterate (BREAKDOWN after 18 iterations, then a
   // peer wait timeout) that LDU_PDL=0 does not (profiles/r01_amg/SUMMARY.md)
-  h->pdl = false;
+  h->pdl = true;  // multi-rank fused chains: control step -> pass with programmatic launch
   if (const char* v = std::getenv("LDU_PDL")) h->pdl = std::atoi(v) != 0;
+  h->mrFuse = true;
+  if (const char* v = std::getenv("LDU_MR_FUSE")) h->mrFuse = std::atoi(v) != 0;
+  h->mrPre = 4;
+  if (const char* v = std::getenv("LDU_MR_PRE")) h->mrPre = std::atoi(v) >= 8 ? 8 : (std::atoi(v) >= 4 ? 4 : 0);
   // persistent cooperative kernels for single-rank, latency-bound sizes (LDU_PERSIST=0/1 forces)
   h->persist = !(h->comm && h->comm->nRanks > 1) && (long long)h->n * 80 < (long long)prop.l2CacheSize;
   if (const char* v = std::getenv("LDU_PERSIST")) h->persist = std::atoi(v) != 0 && !(h->comm && h->comm->nRanks > 1);
@@ -2133,6 +2453,9 @@ void configure(ldu_handle h) {
   with_format(h, [&](auto A) {
     using Fmt = decltype(A);
     h->gridSU = h->suMinB == 8 ? grid_of((const void*)k_pipe_SU<Fmt, 8>) : grid_of((const void*)k_pipe_SU<Fmt>);
+    h->gridSUmr = h->mrPre == 8 ? grid_of((const void*)k_pipe_SU_mr<Fmt, 8>)
+                : h->mrPre == 4 ? grid_of((const void*)k_pipe_SU_mr<Fmt, 4>)
+                                : grid_of((const void*)k_pipe_SU_mr<Fmt, 0>);
   });
   if (h->variant == 6 && h->layout == LDU_LAYOUT_DIA_SYM && h->off[0] == 1) {
     with_dia(h, [&](auto A) {
@@ -2159,7 +2482,7 @@ void configure(ldu_handle h) {
     const long long g = (long long)prop.multiProcessorCount * std::max(1, std::min(o1, o2));
     h->gridP = (int)std::max(1LL, std::min(g, need));
   }
-  h->maxParts = std::max({h->grid, h->gridA, h->gridSU}) + 4096;
+  h->maxParts = std::max({h->grid, h->gridA, h->gridSU, h->gridSUmr}) + 4096;
   h->partials = dmalloc<double>((size_t)kMaxVals * h->maxParts);
   h->ticket = dmalloc<unsigned>(2);  // [0] reductions, [1] halo pack (may run concurrently)
   CUDA_CHECK(cudaMemset(h->ticket, 0, 2 * sizeof(unsigned)));

@@ -70,9 +70,9 @@ def test_poisson_to_tolerance_large(ldu, n, x0kind, norm, solver):
 
 @pytest.mark.parametrize("solver", ["pcg", "pipecg"])
 def test_irregular_sell_to_tolerance_large(ldu, solver):
-    """c5 recipe (exp(0.5 xi) conductances, dropped and diagonal faces, RCM renumbering) at an
-    80^3 base: SELL-32 over > 2 grid-stride wavefronts."""
-    s = meshgen.irregular_mesh(80, seed=1505)
+    """c5 recipe (exp(0.5 xi) conductances, dropped and diagonal faces, RCM renumbering) at a
+    96^3 base (884,736 cells): SELL-32 over > 2 grid-stride wavefronts of every pass."""
+    s = meshgen.irregular_mesh(96, seed=1505)
     ofn = oracle.pcg if solver == "pcg" else oracle.pipecg
     ost, ox, oit, ores = ofn(s, s.b, tol=1e-10, maxIter=20000)
     assert ost == oracle.OK
@@ -90,7 +90,12 @@ def test_irregular_sell_to_tolerance_large(ldu, solver):
 
 @pytest.mark.parametrize("solver,norm", [("pcg", "OpenFOAM"), ("pipecg", "L2")])
 def test_cavity_piso_sequence_512(ldu, solver, norm):
-    """Config 2 semantics at 512^2: 3 time steps x 2 correctors, warm start, tol 1e-6."""
+    """Config 2 semantics at 512^2: 3 time steps x 2 correctors, warm start, tol 1e-6.
+    Bars (DESIGN.md §4 "c2 sequence"): per-solve iteration counts within +-2 %; the final field
+    within 1e-5 of the oracle's (two iterates that both meet a 1e-6 criterion on this
+    Neumann operator, kappa ~ 1e5, may differ by up to kappa * tol; the warm-started sequence of
+    pipelined solves carries the recurrence/true residual gap forward); the GPU's true residual
+    within 10 x tol (L2)."""
     nx = 512
     s = meshgen.cavity_pressure_2d(nx, nx)
     onorm = oracle.NORM_L2 if norm == "L2" else oracle.NORM_OPENFOAM
@@ -111,4 +116,8 @@ def test_cavity_piso_sequence_512(ldu, solver, norm):
                 its_o.append(oit)
     for a, b_ in zip(its, its_o):
         assert abs(a - b_) <= max(1, round(0.02 * b_)), (its, its_o)
-    assert rel(x.cpu().numpy(), xo) <= 1e-6
+    xg = x.cpu().numpy()
+    assert rel(xg, xo) <= 1e-5
+    if norm == "L2":
+        r = b - oracle.amul(s, xg)
+        assert np.linalg.norm(r) / np.linalg.norm(b) <= 10 * 1e-6
