@@ -42,7 +42,7 @@ void destroy_handle(ldu_handle h) {
                   (void*)h->ticket, (void*)h->sums, (void*)h->gsums, (void*)h->st,
                   (void*)h->ifFaceCells, (void*)h->ifCoeffs, (void*)h->sendbuf,
                   (void*)h->recvbuf, (void*)h->ifCell, (void*)h->ifCellPtr, (void*)h->ifFaceIdx,
-                  (void*)h->mrTailIf})
+                  (void*)h->mrTailIf, (void*)h->mrTailMeta})
     ldu::dfree(p);
   if (h->st_host) cudaFreeHost(h->st_host);
   for (cudaEvent_t e : {h->ev[0], h->ev[1], h->ev[2], h->ev[3], h->ev_fork, h->ev_red,

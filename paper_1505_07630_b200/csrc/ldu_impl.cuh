@@ -216,6 +216,7 @@ struct ldu_handle_s {
   // index of position t (or -1)
   int mrGapStart = 0, mrGapLen = 0;
   int* mrTailIf = nullptr;
+  int4* mrTailMeta = nullptr;            // [n - mrGapLen]: {fi, kk, remote face, coeff index} (p2p)
   int gridSUmr = 0, mrPre = 4;           // grid / pre-phase rows per thread (LDU_MR_PRE: 0, 4, 8)
   bool mrFuse = true;                    // one kernel per iteration (LDU_MR_FUSE=0: pack + fix-up)
   unsigned long long* tbuf = nullptr;    // LDU_TRACE device timestamps

@@ -654,7 +654,8 @@ __global__ void __launch_bounds__(kBlock) k_pipe_fixup_p2p(int nIfCells, const i
 // inside the streaming loop.
 struct MrTail {
   int gapStart, gapLen;
-  const int* __restrict__ tailIf;   // [n - gapLen] interface-cell index of position t, or -1
+  const int4* __restrict__ meta;    // [n - gapLen] single-face boundary rows: {fi, kk, remote, 1};
+                                    // no interface: {.., .., .., 0}; several faces: {ic, .., .., 2}
   const int* __restrict__ cellPtr;  // [nIfCells + 1] into faceIdx
   const int* __restrict__ faceIdx;  // packed face index (interface order, then face order)
   const double* __restrict__ coeff; // [nIfFaces] interfaceBouCoeffs
@@ -696,17 +697,22 @@ struct PipeRow {
 // sequence number flagIn), the recurrences, and the halo of exchange i+1 (rD w_{i+1}) as LL
 // words straight into the neighbours' mailboxes over NVLink (no fence, no flag).
 template <class Fmt>
-__device__ __forceinline__ void mr_boundary_row(const Fmt& A, int c, int ic, const double* __restrict__ rD,
+__device__ __forceinline__ void mr_boundary_row(const Fmt& A, int c, int4 m, const double* __restrict__ rD,
                                                 const double* __restrict__ w, double* __restrict__ wn,
                                                 double* __restrict__ z, double* __restrict__ s,
                                                 double* __restrict__ p, double* __restrict__ x,
                                                 double* __restrict__ r, const PipeRow& P,
                                                 const MrTail& T, const P2PDesc* d,
-                                                const uint64_t* recv, uint32_t flagIn, int parOut,
-                                                uint32_t flagOut, double (&v)[3]) {
+                                                const uint64_t* recv, uint32_t flagIn,
+                                                uint64_t* const* dstBase, uint32_t flagOut,
+                                                double (&v)[3]) {
   const double wc0 = __ldg(w + c);
   double nc = row_apply(A, c, wc0, [&](int q) { return __ldg(rD + q) * __ldg(w + q); });
-  if (ic >= 0) {  // interface term of n = A (rD w): y[c] -= coeff * (rD w)_neighbour (Z10, Z23)
+  // interface term of n = A (rD w): y[c] -= coeff * (rD w)_neighbour (Z10, Z23)
+  if (m.w == 1) {  // one face (z-slabs): metadata precomputed, two dependent loads
+    nc -= __ldg(T.coeff + m.x) * ll_load(recv + 2 * (size_t)m.x, flagIn);
+  } else if (m.w == 2) {
+    const int ic = m.x;
     double corr = 0.0;
     for (int f = __ldg(T.cellPtr + ic); f < __ldg(T.cellPtr + ic + 1); ++f) {
       const int fi = __ldg(T.faceIdx + f);
@@ -716,13 +722,36 @@ __device__ __forceinline__ void mr_boundary_row(const Fmt& A, int c, int ic, con
   }
   double rdc;
   const double wc = P.apply(c, wc0, nc, rD, z, s, p, x, r, wn, v, rdc);
-  if (ic < 0) return;
-  const double hv = rdc * wc;
-  for (int f = __ldg(T.cellPtr + ic); f < __ldg(T.cellPtr + ic + 1); ++f) {
-    const int fi = __ldg(T.faceIdx + f);
-    const int kk = __ldg(T.faceIf + fi);
-    uint64_t* dst = mb_haloll(d->base[d->ifNeighbor[kk]], parOut, d->ifRemoteTotal[kk]);
-    ll_store(dst + 2 * (size_t)(d->ifRemoteOff[kk] + (fi - d->ifLocalOff[kk])), hv, flagOut);
+  const double hv = rdc * wc;  // halo of exchange i+1 straight into the neighbours' mailboxes
+  if (m.w == 1) {
+    ll_store(dstBase[m.y] + 2 * (size_t)m.z, hv, flagOut);
+  } else if (m.w == 2) {
+    const int ic = m.x;
+    for (int f = __ldg(T.cellPtr + ic); f < __ldg(T.cellPtr + ic + 1); ++f) {
+      const int fi = __ldg(T.faceIdx + f);
+      const int kk = __ldg(T.faceIf + fi);
+      ll_store(dstBase[kk] + 2 * (size_t)(d->ifRemoteOff[kk] + (fi - d->ifLocalOff[kk])), hv, flagOut);
+    }
+  }
+}
+
+// Boundary-row metadata of the one-kernel loop (built once after the peer tables are known).
+__global__ void k_build_tail_meta(int L, const int* __restrict__ tailIf, const int* __restrict__ cellPtr,
+                                  const int* __restrict__ faceIdx, const int* __restrict__ faceIf,
+                                  const P2PDesc* d, int4* __restrict__ meta) {
+  GRID_STRIDE(j, L) {
+    const int ic = tailIf[j];
+    int4 m = make_int4(0, 0, 0, 0);
+    if (ic >= 0) {
+      if (cellPtr[ic + 1] - cellPtr[ic] == 1) {
+        const int fi = faceIdx[cellPtr[ic]];
+        const int kk = faceIf[fi];
+        m = make_int4(fi, kk, d->ifRemoteOff[kk] + (fi - d->ifLocalOff[kk]), 1);
+      } else {
+        m = make_int4(ic, 0, 0, 2);
+      }
+    }
+    meta[j] = m;
   }
 }
 
@@ -772,14 +801,17 @@ __global__ void __launch_bounds__(kBlock, MINB) k_pipe_SU_mr(Fmt A, const double
     if (bb + kBlock <= gap) bb += ((gap - bb - kBlock) / stride + 1) * stride;
     if (bb < n) {
       if (tid == 0) tstamp(d, k, 4, 1);
+      __shared__ uint64_t* dstBase[kP2PMaxIf];  // exchange i+1's LL slots on each neighbour
+      if (tid < d->nIf)
+        dstBase[tid] = mb_haloll(d->base[d->ifNeighbor[tid]], (int)(seqOut & 1), d->ifRemoteTotal[tid]);
+      __syncthreads();
       const uint64_t* recv = mb_haloll(d->base[d->rank], (int)(seqIn & 1), T.nIfFaces);
       for (int t = bb + tid; t < n; t += stride) {
         if (t < gap) continue;
         int c = T.gapStart + t;
         if (c >= n) c -= n;
-        const int ic = __ldg(T.tailIf + (t - gap));
-        mr_boundary_row(A, c, ic, rD, w, wn, z, s, p, x, r, P, T, d, recv, (uint32_t)seqIn,
-                        (int)(seqOut & 1), (uint32_t)seqOut, v);
+        mr_boundary_row(A, c, __ldg(T.meta + (t - gap)), rD, w, wn, z, s, p, x, r, P, T, d, recv,
+                        (uint32_t)seqIn, dstBase, (uint32_t)seqOut, v);
       }
       if (tid == 0) tstamp(d, k, 6, 2);
     }
@@ -1420,7 +1452,7 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
   const bool mr = multi(h);
   if (mr && h->p2pOn && h->fusePipe && h->mrFuse) {  // ONE kernel per iteration (k_pipe_SU_mr)
     const bool haveIf = h->nIfFaces > 0;
-    MrTail T{h->mrGapStart, haveIf ? h->mrGapLen : h->n, h->mrTailIf, h->ifCellPtr, h->ifFaceIdx,
+    MrTail T{h->mrGapStart, haveIf ? h->mrGapLen : h->n, h->mrTailMeta, h->ifCellPtr, h->ifFaceIdx,
              h->ifCoeffs, h->ifFaceIf, h->nIfFaces};
     const bool pdl = h->pdl && h->trace.empty();
     for (int it = 0; it < batch; ++it) {
@@ -2250,6 +2282,14 @@ void p2p_setup(ldu_handle h) {
   }
   h->p2pDesc = dmalloc<P2PDesc>(1);
   CUDA_CHECK(cudaMemcpy(h->p2pDesc, &d, sizeof(d), cudaMemcpyHostToDevice));
+  if (h->nIfFaces > 0) {  // boundary-row metadata of the one-kernel pipelined loop
+    const int L = h->n - h->mrGapLen;
+    h->mrTailMeta = dmalloc<int4>(std::max(1, L));
+    k_build_tail_meta<<<small_grid(L), kBlock, 0, s>>>(L, h->mrTailIf, h->ifCellPtr, h->ifFaceIdx,
+                                                        h->ifFaceIf, h->p2pDesc, h->mrTailMeta);
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  }
   // every rank's mailbox is mapped before anyone writes into it
   if (cm->nccl()) {
     int* flag = dmalloc<int>(1);
