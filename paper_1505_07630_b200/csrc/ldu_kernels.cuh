@@ -31,19 +31,45 @@ __device__ __forceinline__ double row_apply(const DiaView<ND>& A, int c, double 
   return s;
 }
 
+// SELL-32 row: the slice's pair loads are issued kSellBatch at a time before any gather (no
+// data-dependent exit: a padding entry (col -1, value 0) gathers the row's own operand and adds
+// an exact 0, so the sum of the real entries keeps its order).  One dependent load chain per
+// batch instead of one per pair.
+constexpr int kSellBatch = 4;
 template <class Op>
 __device__ __forceinline__ double row_apply(const SellView& A, int c, double s, Op op) {
   const int slice = c >> 5, lane = c & 31;
   const long long base = __ldg(A.slicePtr + slice);
   const int np = __ldg(A.npairs + slice);
-  for (int jj = 0; jj < np; ++jj) {
+  int jj = 0;
+  for (; jj + kSellBatch <= np; jj += kSellBatch) {
+    int2 cc[kSellBatch];
+    double2 vv[kSellBatch];
+#pragma unroll
+    for (int u = 0; u < kSellBatch; ++u) {
+      const long long e = (base + jj + u) * 32 + lane;
+      cc[u] = __ldg(A.col + e);
+      vv[u] = __ldg(A.val + e);
+    }
+    double x0[kSellBatch], x1[kSellBatch];
+#pragma unroll
+    for (int u = 0; u < kSellBatch; ++u) {
+      x0[u] = op(cc[u].x < 0 ? c : cc[u].x);
+      x1[u] = op(cc[u].y < 0 ? c : cc[u].y);
+    }
+#pragma unroll
+    for (int u = 0; u < kSellBatch; ++u) {
+      s = fma(vv[u].x, x0[u], s);
+      s = fma(vv[u].y, x1[u], s);
+    }
+  }
+  for (; jj < np; ++jj) {
     const long long e = (base + jj) * 32 + lane;
     const int2 cc = __ldg(A.col + e);
     const double2 vv = __ldg(A.val + e);
-    if (cc.x < 0) break;
-    s = fma(vv.x, op(cc.x), s);
-    if (cc.y < 0) break;
-    s = fma(vv.y, op(cc.y), s);
+    const double x0 = op(cc.x < 0 ? c : cc.x), x1 = op(cc.y < 0 ? c : cc.y);
+    s = fma(vv.x, x0, s);
+    s = fma(vv.y, x1, s);
   }
   return s;
 }
