@@ -393,6 +393,48 @@ def rebalance(N: int, r) -> np.ndarray:
     return n
 
 
+def fit_time_model(ns, Ts):
+    """Functional performance model of one device (the paper builds Eq 5's speeds with the
+    FuPerMod functional performance models, "combines the performance model [fupermode]"):
+    T(n) = a + b n, least squares over the measured (cells, seconds per iteration) points.  One
+    point gives a = 0 -- the constant-speed model Eq 5 assumes.  Returns (a, b)."""
+    ns = np.asarray(ns, dtype=F64)
+    Ts = np.asarray(Ts, dtype=F64)
+    if ns.size == 0 or ns.size != Ts.size or np.any(ns <= 0) or np.any(Ts <= 0):
+        raise ValueError("need matching positive sizes and times")
+    if ns.size == 1 or np.ptp(ns) == 0:
+        return 0.0, float(Ts.mean() / ns.mean())
+    b, a = np.polyfit(ns, Ts, 1)
+    if b <= 0:  # not a usable model (noise): fall back to the mean speed
+        return 0.0, float(np.sum(Ts) / np.sum(ns))
+    return float(a), float(b)
+
+
+def fpm_partition(N: int, models, min_cells: int = 1) -> np.ndarray:
+    """Cells per device with equal predicted iteration times under T_i(n) = a_i + b_i n:
+    a_i + b_i n_i = T* for every i and sum_i n_i = N (Eq 7), i.e.
+    T* = (N + sum_i a_i / b_i) / sum_i 1 / b_i,  n_i = (T* - a_i) / b_i,
+    rounded by the largest remainder (as ``rebalance``); a device whose share would fall below
+    ``min_cells`` gets min_cells and the rest is re-solved.  With a_i = 0 this is Eq 5-8."""
+    a = np.array([m[0] for m in models], dtype=F64)
+    b = np.array([m[1] for m in models], dtype=F64)
+    if a.size == 0 or np.any(b <= 0) or N < min_cells * a.size:
+        raise ValueError("bad models or too few cells")
+    fixed = np.zeros(a.size, dtype=bool)
+    n = np.zeros(a.size, dtype=F64)
+    for _ in range(a.size):
+        free = ~fixed
+        rest = N - min_cells * fixed.sum()
+        Tstar = (rest + np.sum(a[free] / b[free])) / np.sum(1.0 / b[free])
+        n[free] = (Tstar - a[free]) / b[free]
+        n[fixed] = min_cells
+        low = free & (n < min_cells)
+        if not low.any():
+            break
+        fixed |= low
+    return rebalance(N, n / n.sum())
+
+
 def slab_bounds_weighted(nCells: int, fractions) -> np.ndarray:
     """Contiguous slabs whose sizes follow Eq 8 for the given work fractions (the weights the
     paper hands to MeTiS/SCOTCH)."""

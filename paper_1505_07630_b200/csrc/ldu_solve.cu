@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(kBlock) k_iface_cg(int nIfCells, const int* __
   finish_reduction<1>(v, rd, st);
 }
 
-enum Pack : int { PACK_PLAIN = 0, PACK_SCALED = 1, PACK_CG_P = 2, PACK_SCALED_W = 3, PACK_SCALED_LL = 4 };
+enum Pack : int { PACK_PLAIN = 0, PACK_SCALED = 1, PACK_CG_P = 2, PACK_SCALED_W = 3, PACK_SCALED_LL = 4,
+                  PACK_SCALED_LL_W = 5 };
 
 // Halo send buffer: the SpMV operand at the interface cells.
 __global__ void k_pack(int nIfFaces, const int* __restrict__ fc, int mode,
@@ -516,12 +517,12 @@ __global__ void __launch_bounds__(kBlock) k_pack_p2p(int nIfFaces, const int* __
   }
   const unsigned long long seq = d->seqHaloSend + 1;
   const int par = (int)(seq & 1);
-  if (mode == PACK_SCALED_W) a = (k & 1) ? p0 : p1;  // w_{i+1} written by the fused pass i
-  const bool ll = mode == PACK_SCALED_LL;
+  if (mode == PACK_SCALED_W || mode == PACK_SCALED_LL_W) a = (k & 1) ? p0 : p1;  // w_{i+1}
+  const bool ll = mode == PACK_SCALED_LL || mode == PACK_SCALED_LL_W;
   GRID_STRIDE(i, nIfFaces) {
     const int c = fc[i];
     double v = a[c];
-    if (mode == PACK_SCALED || mode == PACK_SCALED_W || ll) v = rD[c] * v;
+    if (mode == PACK_SCALED || mode == PACK_SCALED_W || ll) v = rD[c] * v;  // rD w
     else if (mode == PACK_CG_P) v = fma(beta, pold[c], rD[c] * v);
     const int kk = faceIf[i];
     if (ll) {  // exchange 0 of the one-kernel loop: LL words, no flag (the flag release is skipped)
@@ -877,14 +878,17 @@ __global__ void __launch_bounds__(kBlock, MINB) k_pipe_SU_mr(Fmt A, const double
 // Control step of the one-kernel loop: gather iteration i-1's sums from the LL slots of this
 // rank's mailbox (lane q polls rank q), sum them in rank order, run CTL_PIPE_NEXT.  The first
 // trip (k = -1) gathers the init's reduction, published with the flag protocol.
-__global__ void k_ctl_ll(State* st, P2PDesc* d) {
+// flagFirst = 1: this trip gathers a reduction published with the flag protocol (the first
+// trip after a residual replacement).
+__global__ void k_ctl_ll(State* st, P2PDesc* d, int flagFirst) {
   pdl_wait();
   pdl_trigger();  // the pass may launch now and run its pre-phase while we wait
   if (st->done) return;
   __shared__ double part[kP2PMaxRanks][3];
   const int lane = threadIdx.x;
   const unsigned long long sq = d->seqRed + 1;
-  if (st->k >= 0) {
+  const bool ll = st->k >= 0 && !flagFirst;
+  if (ll) {
     char* me = d->base[d->rank];
     for (int q = lane; q < d->nRanks; q += blockDim.x) {
       const uint64_t* src = mb_redll(me, (int)(sq & 1), q);
@@ -896,7 +900,7 @@ __global__ void k_ctl_ll(State* st, P2PDesc* d) {
   if (lane != 0) return;
   tstamp(d, st->k + 1, 0, 0);
   double sums[kMaxVals] = {0.0, 0.0, 0.0, 0.0};
-  if (st->k >= 0) {
+  if (ll) {
     for (int q = 0; q < d->nRanks; ++q)
       for (int m = 0; m < 3; ++m) sums[m] += part[q][m];
     d->seqRed = sq;
@@ -904,9 +908,34 @@ __global__ void k_ctl_ll(State* st, P2PDesc* d) {
     p2p_gather_sums<kMaxVals>(d, sums);
   }
   tstamp(d, st->k + 1, 1, 0);
-  if (d->nIf > 0 && st->k >= 0) d->seqHalo += 1;  // exchange i-1, consumed by pass i-1
+  // exchange i-1, consumed by pass i-1 (after a replacement the drain retired it already)
+  if (d->nIf > 0 && st->k >= 0 && !flagFirst) d->seqHalo += 1;
   run_ctl(CTL_PIPE_NEXT, st, sums);
   if (d->nIf > 0 && st->done) d->seqHalo += 1;    // exchange i, sent by pass i-1, never read
+}
+
+// Residual replacement in the one-kernel loop (NEXT-4): the sums of the pass just before the
+// replacement are superseded -- drain them (every rank published them), retire that pass's
+// consumed exchange and its unread outgoing one.
+__global__ void k_ctl_ll_drain(State* st, P2PDesc* d) {
+  if (st->done) return;
+  const unsigned long long sq = d->seqRed + 1;
+  char* me = d->base[d->rank];
+  for (int q = threadIdx.x; q < d->nRanks; q += blockDim.x) {
+    const uint64_t* src = mb_redll(me, (int)(sq & 1), q);
+    for (int m = 0; m < 3; ++m) (void)ll_load(src + 2 * m, (uint32_t)sq);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    d->seqRed = sq;
+    if (d->nIf > 0) d->seqHalo += 2;
+  }
+}
+
+// y = rD . x (residual replacement operands)
+__global__ void k_scale_rD(int n, const double* __restrict__ rD, const double* __restrict__ x,
+                           double* __restrict__ y) {
+  GRID_STRIDE(c, n) y[c] = rD[c] * x[c];
 }
 
 // The fused multi-rank loop starts at k = -1 (its first control step evaluates i = 0).
@@ -1252,8 +1281,9 @@ void p2p_join(ldu_handle h, cudaStream_t s) { CUDA_CHECK(cudaStreamWaitEvent(s, 
 // classical loop and the first exchange of the fused loop) reads the live State, which nothing
 // modifies concurrently there; GATE_NONE (amul_dev) always sends -- its consumer always reads.
 void p2p_pack(ldu_handle h, int mode, const double* a, cudaStream_t s, int gate) {
-  const double* q0 = mode == PACK_SCALED_W ? h->w : h->p0;
-  const double* q1 = mode == PACK_SCALED_W ? h->w2 : h->p1;
+  const bool wpair = mode == PACK_SCALED_W || mode == PACK_SCALED_LL_W;
+  const double* q0 = wpair ? h->w : h->p0;
+  const double* q1 = wpair ? h->w2 : h->p1;
   const int *gk = nullptr, *gd = nullptr;
   if (gate == GATE_SNAP) {
     gk = &h->p2pDesc->snapK;
@@ -1447,7 +1477,8 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
   return kernels;
 }
 
-long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profile) {
+long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profile,
+                             bool rrFirst = false) {
   long long kernels = 0;
   const bool mr = multi(h);
   if (mr && h->p2pOn && h->fusePipe && h->mrFuse) {  // ONE kernel per iteration (k_pipe_SU_mr)
@@ -1457,7 +1488,8 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
     const bool pdl = h->pdl && h->trace.empty();
     for (int it = 0; it < batch; ++it) {
       trace_mark(h, it, 0, s);
-      launch_pdl(pdl && it > 0 && !profile, k_ctl_ll, 1, 64, s, h->st, h->p2pDesc);
+      launch_pdl(pdl && it > 0 && !profile, k_ctl_ll, 1, 64, s, h->st, h->p2pDesc,
+                 (rrFirst && it == 0) ? 1 : 0);
       ++kernels;
       trace_mark(h, it, 1, s);
       prof_mark(h, profile, 4 * it + 0, s);
@@ -1648,6 +1680,14 @@ __global__ void __launch_bounds__(kBlock) k_rr_w(Fmt A, const double* __restrict
   }
 }
 
+// w_{i+1} = y (A rD r incl. interfaces) into the ping-pong half the next fused pass reads
+__global__ void __launch_bounds__(kBlock) k_rr_copy_w(int n, const double* __restrict__ y,
+                                                      double* w0, double* w1, const State* st) {
+  if (st->done) return;
+  double* __restrict__ wn = (st->k & 1) ? w0 : w1;
+  GRID_STRIDE(c, n) wn[c] = y[c];
+}
+
 // the iteration's fused reduction over the replaced vectors: [(r, rD.r), (w, rD.r), crit(r)]
 __global__ void __launch_bounds__(kBlock) k_rr_dots(int n, const double* __restrict__ rD,
                                                     const double* __restrict__ r, const double* w0,
@@ -1693,6 +1733,36 @@ long long enqueue_pipe_rr(ldu_handle h, int batch, cudaStream_t s, bool profile)
   k_rr_dots<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->r, h->w, h->w2, h->st,
                                        red_of(h, CTL_PIPE_NEXT, true));
   return kernels + 6;
+}
+
+// Multi-rank residual replacement (one-kernel loop): `batch` fused iterations, then r = b - A x,
+// w = A rD r, s = A p, z = A rD s with their halo exchanges (amul_dev), the reduction of the
+// replaced vectors (flag protocol; the next batch's first control step gathers it) and the halo
+// of rD w sent as exchange 0 of the next batch -- the single-rank replacement with the
+// interfaces included (GV 2014 Sec. 4 [ext]; reading Z7).
+long long enqueue_pipe_rr_mr(ldu_handle h, int batch, cudaStream_t s, bool profile) {
+  long long kernels = enqueue_pipe_iters(h, batch, s, profile, true);
+  k_ctl_ll_drain<<<1, 64, 0, s>>>(h->st, h->p2pDesc);
+  ++kernels;
+  double* tmp = h->nv;
+  // w_{i+1} lives in the ping-pong half the next pass reads: (k & 1) ? w : w2 after pass k; the
+  // graph is fixed, so both halves are written in turn by parity-selecting kernels
+  amul_dev(h, h->x, h->ybuf, s, kernels);
+  k_rr_r<<<h->grid, kBlock, 0, s>>>(h->n, h->bbuf, h->ybuf, h->r, h->st);
+  k_scale_rD<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->r, tmp);
+  amul_dev(h, tmp, h->ybuf, s, kernels);
+  k_rr_copy_w<<<h->grid, kBlock, 0, s>>>(h->n, h->ybuf, h->w, h->w2, h->st);
+  amul_dev(h, h->p0, h->s, s, kernels);
+  k_scale_rD<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->s, tmp);
+  amul_dev(h, tmp, h->z, s, kernels);
+  k_rr_dots<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->r, h->w, h->w2, h->st,
+                                       red_loop(h, CTL_NONE, false));
+  kernels += 5;
+  if (h->nIfFaces) {  // exchange of the replaced rD w for the next pass (LL words)
+    p2p_pack(h, PACK_SCALED_LL_W, nullptr, s, GATE_LIVE);
+    ++kernels;
+  }
+  return kernels;
 }
 
 }  // namespace
@@ -1754,8 +1824,9 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   if (o.replaceEvery < 0) fail_arg("replaceEvery must be >= 0");
   const int rr = o.replaceEvery;
   if (rr && !pipelined) fail_arg("replaceEvery applies to pipelined CG only");
-  if (rr && (multi(h) || !h->fusePipe))
-    throw Error(LDU_ERR_STATE, "residual replacement needs the single-rank fused pipelined pass");
+  if (rr && (!h->fusePipe || (multi(h) && !(h->p2pOn && h->mrFuse))))
+    throw Error(LDU_ERR_STATE, "residual replacement needs the fused pipelined pass (single rank, "
+                               "or the one-kernel multi-rank loop)");
   const bool profile = o.profile == 1;
   const int batch = rr ? rr : (o.batch ? o.batch : 32);
 
@@ -1996,7 +2067,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     const ldu_solve_stats saved = h->stats;  // capture enqueues nothing that runs now
     cudaGraph_t g;
     CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    G.kernels = rr ? enqueue_pipe_rr(h, batch, s, profile)
+    G.kernels = rr ? (mr ? enqueue_pipe_rr_mr(h, batch, s, profile) : enqueue_pipe_rr(h, batch, s, profile))
                    : pipelined ? enqueue_pipe_iters(h, batch, s, profile)
                                : enqueue_cg_iters(h, batch, s, profile);
     CUDA_CHECK(cudaStreamEndCapture(s, &g));

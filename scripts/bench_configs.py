@@ -355,6 +355,11 @@ def c5dist(ldu, n=160, iters=200, slow_rank_sms=None):
     # a second application of Eq 5-8 from the re-decomposed run's own times
     s = [meshgen.speed(nc, nf, kms) for kms, nc, nf in ks2]
     run(meshgen.slab_bounds_weighted(g.nCells, meshgen.relative_speeds(s)), "Eq 5-8, second pass")
+    # functional performance model (FuPerMod): T_i(n) = a_i + b_i n fitted per rank from
+    # its two measured sizes (equal cells, Eq 5-8), then equal predicted times (meshgen.fpm_partition)
+    models = [meshgen.fit_time_model([k1[1], k2[1]], [k1[0], k2[0]]) for k1, k2 in zip(ks, ks2)]
+    n_fpm = meshgen.fpm_partition(g.nCells, models)
+    run(np.concatenate([[0], np.cumsum(n_fpm)]).astype(np.int64), "FPM fitted T(n) = a + b n (2 points)")
     comm.close()
     dist.destroy_process_group()
 

@@ -20,6 +20,19 @@ import torch.distributed as dist  # noqa: E402
 import meshgen  # noqa: E402
 
 
+def slab_bounds_for(g, world):
+    """LDU_DIST_BOUNDS: equal (default) cell slabs, Eq 5-8 weighted slabs (work
+    fractions proportional to 1, 2, .., world -- a heterogeneous set of speeds), or slabs with
+    equal non-zeros (meshgen.nnz_balanced_bounds, NEXT-3)."""
+    mode = os.environ.get("LDU_DIST_BOUNDS", "equal")
+    if mode == "weighted":
+        r = meshgen.relative_speeds(np.arange(1, world + 1, dtype=float))
+        return meshgen.slab_bounds_weighted(g.nCells, r)
+    if mode == "nnz":
+        return meshgen.nnz_balanced_bounds(g, world)
+    return meshgen.slab_bounds(g.nCells, world)
+
+
 def stress(rank, world, comm, ldu):
     """Repeated fused pipelined solves (>= 10^4 iterations in total on two mesh sizes): every
     repeat bitwise equal to the first, the first equal to the oracle."""
@@ -90,9 +103,9 @@ def main():
     ok = True
     for name, mk in cases.items():
         g = mk()
-        parts = meshgen.slab_partition(g, world)
+        bounds = slab_bounds_for(g, world)
+        parts = meshgen.slab_partition(g, world, bounds=bounds)
         me = parts[rank]
-        bounds = meshgen.slab_bounds(g.nCells, world)
         lo, hi = int(bounds[rank]), int(bounds[rank + 1])
         A = ldu.LduMatrix.from_system(me, comm)
         xg = np.random.default_rng(5).uniform(-1, 1, g.nCells)
@@ -121,6 +134,12 @@ def main():
             sto, ito, reso = fn(b, xo, tol=1e-6, maxIter=5000, norm=ldu.NORM_OPENFOAM,
                                 relTol=0.01, minIter=3, record_history=True)
             out[solver + "_of"] = (sto, ito, reso, xo.cpu().numpy(), A.history())
+            if solver == "pipecg" and os.environ.get("LDU_PIPE_FUSE", "1") != "0":
+                # residual replacement every 25 iterations across ranks (NEXT-4, reading Z7)
+                xr = torch.zeros_like(b)
+                str_, itr, resr = fn(b, xr, tol=1e-10, maxIter=5000, replaceEvery=25,
+                                     record_history=True)
+                out["pipecg_rr"] = (str_, itr, resr, xr.cpu().numpy(), A.history())
         A.close()
         gathered = [None] * world
         dist.all_gather_object(gathered, out)
@@ -166,6 +185,20 @@ def main():
                                                rel=rel_of, history_ok=bool(hist_ok))
                 ok &= {o[0] for o in of} == {0} and {o[1] for o in of} == {oit2}
                 ok &= rel_of <= 1e-8 and hist_ok
+            if "pipecg_rr" in gathered[0]:
+                ost3, ox3, oit3, ores3, ohist3 = oracle.pipecg(g, g.b, tol=1e-10, maxIter=5000,
+                                                               history=True, replace_every=25)
+                rr = [o["pipecg_rr"] for o in gathered]
+                x_rr = np.concatenate([o[3] for o in rr])
+                rel_rr = float(np.linalg.norm(x_rr - ox3) / np.linalg.norm(ox3))
+                h3 = rr[0][4]
+                m3 = min(len(h3), len(ohist3), 60)
+                hist_rr = bool(np.allclose(h3[:m3], ohist3[:m3], rtol=1e-7))
+                r["pipecg_replace25"] = dict(iters=sorted({o[1] for o in rr}), oracle_iters=oit3,
+                                             rel=rel_rr, history_ok=hist_rr)
+                ok &= {o[0] for o in rr} == {0} and len({o[1] for o in rr}) == 1
+                ok &= abs(rr[0][1] - oit3) <= max(1, round(0.02 * oit3))
+                ok &= rel_rr <= 1e-8 and hist_rr
             results[name] = r
     comm.close()
     dist.barrier()

@@ -57,3 +57,45 @@ def test_nnz_balanced_bounds():
     loads = np.array([w[b[g]:b[g + 1]].sum() for g in range(p)])
     assert b[0] == 0 and b[-1] == N and np.all(np.diff(b) > 0)
     assert loads.max() - loads.min() <= 2 * w.max()
+
+
+# ---- functional performance model (FuPerMod, the paper's reference for Eq 5; NEXT-3) -----------
+def test_fpm_single_point_is_eq5_to_eq8():
+    """One measurement per device (a = 0): the FPM partition is exactly Eq 5-8."""
+    ns = [250_000, 250_000, 250_000, 250_000]
+    Ts = [0.004, 0.001, 0.002, 0.0013]
+    models = [meshgen.fit_time_model([n], [T]) for n, T in zip(ns, Ts)]
+    assert all(a == 0.0 for a, _ in models)
+    fp = meshgen.fpm_partition(1_000_000, models)
+    eq8 = meshgen.rebalance(1_000_000, meshgen.relative_speeds(
+        [meshgen.speed(n, 0, T) for n, T in zip(ns, Ts)]))
+    np.testing.assert_array_equal(fp, eq8)
+
+
+def test_fpm_equalises_affine_devices_where_eq8_overshoots():
+    """Devices with a fixed per-iteration cost (T_i(n) = a_i + b_i n): Eq 5-8 from one
+    measurement leaves the times unequal (the one-shot re-decomposition over-corrects, as
+    measured in r01); the model fitted from two measurements equalises them up to rounding."""
+    a = np.array([20e-6, 15e-6, 15e-6, 15e-6])
+    b = np.array([25e-12, 14e-12, 14e-12, 14e-12])
+    T = lambda n: a + b * n  # noqa: E731
+    N = 4_096_000
+    n0 = meshgen.slab_bounds(N, 4)
+    n0 = np.diff(n0)
+    eq8 = meshgen.rebalance(N, meshgen.relative_speeds(n0 / T(n0)))
+    t8 = T(eq8)
+    models = [meshgen.fit_time_model([n0[i], eq8[i]], [T(n0)[i], t8[i]]) for i in range(4)]
+    for (ai, bi), at, bt in zip(models, a, b):
+        assert abs(ai - at) <= 1e-12 and abs(bi - bt) <= 1e-18
+    fp = meshgen.fpm_partition(N, models)
+    tf = T(fp)
+    assert fp.sum() == N
+    assert tf.max() / tf.min() < 1 + 1e-5          # equal up to the rounding of cells
+    assert t8.max() / t8.min() > 1.05              # Eq 8 alone: several % apart
+    assert tf.max() < t8.max()                     # so the step time improves
+
+
+def test_fpm_min_cells_clamp():
+    models = [(1.0, 1e-6), (0.0, 1e-6), (0.0, 1e-6)]  # device 0: a fixed cost above the balance
+    n = meshgen.fpm_partition(1000, models, min_cells=5)
+    assert n.sum() == 1000 and n[0] == 5 and abs(int(n[1]) - int(n[2])) <= 1

@@ -86,6 +86,17 @@ def test_distributed_parity_shared_gpu(nproc, mode):
     assert p.returncode == 0 and "DIST_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
 
 
+@pytest.mark.parametrize("bounds,nproc", [("weighted", 2), ("weighted", 3), ("nnz", 3)])
+def test_distributed_unequal_slabs_shared_gpu(bounds, nproc):
+    """NEXT-3 through the library: Eq 5-8 weighted slabs (work fractions 1 : 2 : .. : nproc)
+    and equal-non-zero slabs of every case (incl. the irregular RCM mesh, whose slab boundaries
+    are ragged) -- the one-kernel loop's interface-free run and boundary rows on unequal ranks."""
+    p = _torchrun(nproc, 29591 + nproc + (10 if bounds == "nnz" else 0),
+                  [os.path.join(ROOT, "tests", "dist_worker.py")],
+                  {"LDU_DIST_BOOT": "host", "LDU_DIST_BOUNDS": bounds})
+    assert p.returncode == 0 and "DIST_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
 @pytest.mark.parametrize("nproc", [2, 4])
 def test_distributed_amg_parity_shared_gpu(nproc):
     p = _torchrun(nproc, 29551 + nproc, [os.path.join(ROOT, "tests", "dist_amg_worker.py")],
