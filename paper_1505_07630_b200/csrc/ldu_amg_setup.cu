@@ -965,6 +965,250 @@ __global__ void k_expand_RAP(CsrView R, CsrView Q, int nc, int r0, int r1,
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Row-wise SpGEMM C = A B with a per-warp hash accumulator (one warp per output row).
+// Row I of C is accumulated in the expansion order of the sort-based assembly (A's entries t
+// ascending, then B_j's entries ascending): the warp walks A's row entry by entry; the lanes take
+// the entries of B_j (distinct columns, so every accumulator slot gets at most one addend per
+// step) and __syncwarp orders the steps -- each C_IJ is the same sequential sum, bit for bit, as
+// assemble()'s stable radix sort + segmented sum, without expanding or sorting the products.
+// A row with more than CAP distinct columns overflows: the caller retries with a larger CAP,
+// then falls back to the sort path.
+// ---------------------------------------------------------------------------------------------
+struct PhaseTrace;
+void sub_mark(const char* what);
+constexpr int kGemmWarps = 4;   // warps per block (CAP = 512: 32 KB of shared memory)
+
+struct BCsr {  // B as CSR
+  CsrView m;
+  __device__ __forceinline__ int begin(int j) const { return __ldg(m.ptr + j); }
+  __device__ __forceinline__ int end(int j) const { return __ldg(m.ptr + j + 1); }
+  __device__ __forceinline__ int col(int u, int) const { return __ldg(m.col + u); }
+  __device__ __forceinline__ double val(int u) const { return __ldg(m.val + u); }
+};
+struct BAgg {  // B = T, the aggregate indicator: row j = {(agg[j], 1)}
+  const int* __restrict__ agg;
+  __device__ __forceinline__ int begin(int j) const { return j; }
+  __device__ __forceinline__ int end(int j) const { return j + 1; }
+  __device__ __forceinline__ int col(int u, int) const { return __ldg(agg + u); }
+  __device__ __forceinline__ double val(int) const { return 1.0; }
+};
+
+// WRITE = false: cnt[I] = number of (non-zero, when drop) entries of row I; *overflow set when a
+// row does not fit.  WRITE = true: the row's entries in ascending column order at ptr[I].
+// G lanes per output row (32 / G rows per warp, each group with its own CAP-slot table).
+template <class B, bool WRITE, int CAP, int G>
+__global__ void __launch_bounds__(kGemmWarps * 32) k_spgemm_rows(CsrView A, B b, int drop,
+                                                                 int* __restrict__ cnt,
+                                                                 const int* __restrict__ ptr,
+                                                                 int* __restrict__ ocol,
+                                                                 double* __restrict__ oval,
+                                                                 int* __restrict__ overflow) {
+  static_assert((CAP & (CAP - 1)) == 0 && CAP >= G, "CAP: a power of two >= G");
+  static_assert(G == 4 || G == 8 || G == 16 || G == 32, "G: 4, 8, 16 or 32 lanes per row");
+  constexpr int LOG2 = CAP == 16 ? 4 : CAP == 32 ? 5 : CAP == 64 ? 6 : CAP == 128 ? 7 : CAP == 256 ? 8 : 9;
+  constexpr int RPW = 32 / G;  // rows per warp
+  __shared__ int keys[kGemmWarps * RPW][CAP];
+  __shared__ double acc[kGemmWarps * RPW][CAP];
+  __shared__ int lst[kGemmWarps * RPW][CAP];
+  const int lane = threadIdx.x & 31, sub = lane % G, grp = (threadIdx.x >> 5) * RPW + lane / G;
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u) << ((lane / G) * G));
+  int* K = keys[grp];
+  double* V = acc[grp];
+  int* L = lst[grp];
+  const int rowsPerPass = gridDim.x * kGemmWarps * RPW;
+  const int first = (blockIdx.x * kGemmWarps + (threadIdx.x >> 5)) * RPW + lane / G;
+  const int trips = (A.n + rowsPerPass - 1) / rowsPerPass;  // group-uniform trip count
+  for (int trip = 0; trip < trips; ++trip) {
+    const int I = first + trip * rowsPerPass;
+    const bool live = I < A.n;
+    for (int q = sub; q < CAP; q += G) {
+      K[q] = -1;
+      V[q] = 0.0;
+    }
+    __syncwarp(gmask);
+    bool full = false;
+    const int t0 = live ? __ldg(A.ptr + I) : 0, t1 = live ? __ldg(A.ptr + I + 1) : 0;
+    for (int tb = t0; tb < t1; tb += G) {  // A's entries G at a time: one load round trip
+      const int tl = tb + sub;
+      int jl = 0, bl = 0, el = 0;
+      double al = 0.0;
+      if (tl < t1) {
+        jl = __ldg(A.col + tl);
+        al = __ldg(A.val + tl);
+        bl = b.begin(jl);
+        el = b.end(jl);
+      }
+      const int tn = min(G, t1 - tb);
+      for (int q = 0; q < tn; ++q) {  // group-uniform: A's entries in order
+        const int j = __shfl_sync(gmask, jl, q, G);
+        const double a = __shfl_sync(gmask, al, q, G);
+        const int ub = __shfl_sync(gmask, bl, q, G), ue = __shfl_sync(gmask, el, q, G);
+        for (int u = ub + sub; u < ue; u += G) {
+          const int c = b.col(u, j);
+          unsigned h = ((unsigned)c * 2654435761u) >> (32 - LOG2);
+          int probes = 0;
+          while (true) {
+            const int prev = atomicCAS(&K[h], -1, c);
+            if (prev == -1 || prev == c) break;
+            h = (h + 1) & (CAP - 1);
+            if (++probes == CAP) {
+              full = true;
+              break;
+            }
+          }
+          if (full) break;
+          V[h] += a * b.val(u);  // one addend per slot per step (B_j's columns are distinct)
+        }
+        __syncwarp(gmask);
+      }
+    }
+    if (__any_sync(gmask, full)) {
+      if (sub == 0) atomicExch(overflow, 1);
+      if (!WRITE && sub == 0 && live) cnt[I] = 0;
+      __syncwarp(gmask);
+      continue;
+    }
+    // compact the kept entries (key set, value non-zero when dropping) into L
+    int m = 0;
+    for (int q0 = 0; q0 < CAP; q0 += G) {
+      const int q = q0 + sub;
+      const bool keep = K[q] >= 0 && !(drop && V[q] == 0.0);
+      const unsigned bal = __ballot_sync(gmask, keep) >> ((lane / G) * G);
+      if (keep) L[m + __popc(bal & ((1u << sub) - 1))] = q;
+      m += __popc(bal);
+    }
+    __syncwarp(gmask);
+    if (sub == 0 && live && cnt) cnt[I] = m;
+    if (!WRITE) {
+      __syncwarp(gmask);
+      continue;
+    }
+    if (live) {
+      const int base = __ldg(ptr + I);
+      for (int e = sub; e < m; e += G) {  // rank by counting: ascending column order
+        const int q = L[e], c = K[q];
+        int rank = 0;
+        for (int f = 0; f < m; ++f) rank += K[L[f]] < c;
+        ocol[base + rank] = c;
+        oval[base + rank] = V[q];
+      }
+    }
+    __syncwarp(gmask);
+  }
+}
+
+__global__ void k_i2l(long long n, const int* __restrict__ a, long long* __restrict__ b) {
+  GSTRIDE(i, n) b[i] = a[i];
+}
+
+// per-row bound of C's row length: min(expansion size, CAP)
+template <class B>
+__global__ void k_expansion_bound(CsrView A, B b, int cap, long long* __restrict__ ub) {
+  GSTRIDE(I, A.n) {
+    long long e = 0;
+    for (int t = A.ptr[I]; t < A.ptr[I + 1]; ++t) {
+      const int j = A.col[t];
+      e += b.end(j) - b.begin(j);
+    }
+    ub[I] = e < cap ? e : cap;
+  }
+}
+
+// copy row I's cnt[I] entries from the bound-spaced scratch to the packed CSR (a warp per row)
+__global__ void k_compact_rows(int rows, const long long* __restrict__ toff, const int* __restrict__ tcol,
+                               const double* __restrict__ tval, const int* __restrict__ ptr,
+                               int* __restrict__ col, double* __restrict__ val) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < rows; r += nwarps) {
+    const long long src = toff[r];
+    const int dst = ptr[r], m = ptr[r + 1] - dst;
+    for (int e = lane; e < m; e += 32) {
+      col[dst + e] = tcol[src + e];
+      val[dst + e] = tval[src + e];
+    }
+  }
+}
+
+// C = A B (nrows = A.n, ncols) by k_spgemm_rows in ONE pass: every row's sorted entries go to a
+// scratch spaced by the row bound min(expansion, CAP), then are packed; returns false (C
+// untouched) when a row overflows CAP
+template <class B, int CAP, int G>
+bool spgemm_rows_cap(const CsrMat& A, B b, int ncols, bool drop, CsrMat& C, cudaStream_t s) {
+  Scratch sc(s);
+  const int n = A.nrows;
+  long long* ub = sc.get<long long>(n + 1);
+  long long* toff = sc.get<long long>(n + 1);
+  k_expansion_bound<<<nblk(n), kSB, 0, s>>>(view(A), b, CAP, ub);
+  exclusive_scan<long long>(ub, toff, n, s);
+  const long long tot = d2h(toff + n, s);
+  int* tcol = sc.get<int>(std::max(1LL, tot));
+  double* tval = sc.get<double>(std::max(1LL, tot));
+  int* cnt = sc.get<int>(n + 1);
+  int* ovf = sc.get<int>(1);
+  CUDA_CHECK(cudaMemsetAsync(ovf, 0, sizeof(int), s));
+  // the kernel writes at int offsets: scratch offsets beyond 2^31 take the two-pass route below
+  static const bool twoPass = std::getenv("LDU_AMG_GEMM_2PASS") && std::atoi(std::getenv("LDU_AMG_GEMM_2PASS")) != 0;
+  const bool onePass = tot < (1LL << 31) - 1 && !twoPass;
+  int* toff32 = nullptr;
+  if (onePass) {
+    toff32 = sc.get<int>(n + 1);
+    k_l2i<<<nblk(n + 1), kSB, 0, s>>>(n + 1, toff, toff32);
+  }
+  constexpr int rpb = kGemmWarps * (32 / G);
+  const int grid = (int)std::max(1LL, std::min<long long>((n + rpb - 1) / rpb, 148LL * 16));
+  if (onePass)
+    k_spgemm_rows<B, true, CAP, G><<<grid, kGemmWarps * 32, 0, s>>>(view(A), b, drop ? 1 : 0, cnt,
+                                                                    toff32, tcol, tval, ovf);
+  else
+    k_spgemm_rows<B, false, CAP, G><<<grid, kGemmWarps * 32, 0, s>>>(view(A), b, drop ? 1 : 0, cnt,
+                                                                     nullptr, nullptr, nullptr, ovf);
+  CUDA_CHECK(cudaGetLastError());
+  sub_mark("gemm rows");
+  if (d2h(ovf, s)) return false;
+  long long* cl = sc.get<long long>(n + 1);
+  long long* off64 = sc.get<long long>(n + 1);
+  k_i2l<<<nblk(n), kSB, 0, s>>>(n, cnt, cl);
+  exclusive_scan<long long>(cl, off64, n, s);
+  const long long nnz = d2h(off64 + n, s);
+  if (nnz >= (1LL << 31) - 1) throw Error(LDU_ERR_OOM, "AMG level exceeds 2^31 stored entries");
+  C = CsrMat();
+  C.nrows = n;
+  C.ncols = ncols;
+  C.nnz = nnz;
+  C.ptr = dmalloc<int>(n + 1);
+  C.col = dmalloc<int>(nnz);
+  C.val = dmalloc<double>(nnz);
+  k_l2i<<<nblk(n + 1), kSB, 0, s>>>(n + 1, off64, C.ptr);
+  if (onePass) {
+    const int g2 = (int)std::max(1LL, std::min<long long>(((long long)n * 32 + kSB - 1) / kSB, 148LL * 64));
+    k_compact_rows<<<g2, kSB, 0, s>>>(n, toff, tcol, tval, C.ptr, C.col, C.val);
+  } else {
+    k_spgemm_rows<B, true, CAP, G><<<grid, kGemmWarps * 32, 0, s>>>(view(A), b, drop ? 1 : 0,
+                                                                    nullptr, C.ptr, C.col, C.val, ovf);
+  }
+  CUDA_CHECK(cudaGetLastError());
+  sub_mark("gemm pack");
+  C.group = group_of(C.nnz, n);
+  return true;
+}
+
+// narrow B rows (the aggregate indicator, P): 4 / 8 lanes per row; wide (A P): a warp per row
+template <class B>
+bool spgemm_rows(const CsrMat& A, B b, int ncols, bool drop, bool narrow, CsrMat& C, cudaStream_t s) {
+  static const bool off = std::getenv("LDU_AMG_SORT_GEMM") && std::atoi(std::getenv("LDU_AMG_SORT_GEMM")) != 0;
+  if (off) return false;
+  if (narrow)
+    return spgemm_rows_cap<B, 32, 4>(A, b, ncols, drop, C, s) ||
+           spgemm_rows_cap<B, 64, 8>(A, b, ncols, drop, C, s) ||
+           spgemm_rows_cap<B, 256, 32>(A, b, ncols, drop, C, s) ||
+           spgemm_rows_cap<B, 512, 32>(A, b, ncols, drop, C, s);
+  return spgemm_rows_cap<B, 128, 32>(A, b, ncols, drop, C, s) ||
+         spgemm_rows_cap<B, 512, 32>(A, b, ncols, drop, C, s);
+}
+
 CsrMat build_P(const CsrMat& A, const int* agg, int nAgg, const double* diag, double omega,
                bool smooth, cudaStream_t s) {
   Scratch sc(s);
@@ -975,41 +1219,112 @@ CsrMat build_P(const CsrMat& A, const int* agg, int nAgg, const double* diag, do
     k_expand_T<<<nblk(n), kSB, 0, s>>>(n, nAgg, agg, key, val);
     return assemble(n, nAgg, n, key, val, false, s);
   }
-  CsrMat P = assemble_rows(  // S = A T
-      n, nAgg, false, s, [&](long long* cnt) { k_count_row<<<nblk(n), kSB, 0, s>>>(view(A), cnt); },
-      [&](int r0, int r1, const long long* off, unsigned long long* key, double* val) {
-        k_expand_AT<<<nblk(r1 - r0), kSB, 0, s>>>(view(A), nAgg, agg, r0, r1, off, key, val);
-      });
+  CsrMat P;  // S = A T
+  if (!spgemm_rows(A, BAgg{agg}, nAgg, false, true, P, s))
+    P = assemble_rows(
+        n, nAgg, false, s, [&](long long* cnt) { k_count_row<<<nblk(n), kSB, 0, s>>>(view(A), cnt); },
+        [&](int r0, int r1, const long long* off, unsigned long long* key, double* val) {
+          k_expand_AT<<<nblk(r1 - r0), kSB, 0, s>>>(view(A), nAgg, agg, r0, r1, off, key, val);
+        });
   int* zeros = sc.get<int>(1);
   CUDA_CHECK(cudaMemsetAsync(zeros, 0, sizeof(int), s));
   k_finish_P<<<nblk(n), kSB, 0, s>>>(view(P), agg, diag, omega, P.val, zeros);
   CUDA_CHECK(cudaGetLastError());
   if (d2h(zeros, s)) drop_zeros(P, s);
+  sub_mark("finish P");
   return P;
 }
 
+// Transpose by counting: column counts, scan, scatter through per-column cursors (arbitrary
+// order), then every row of the transpose sorted by its (distinct) column indices -- a warp per
+// row, rank by counting: deterministic, and equal to the stable-sort transpose.
+__global__ void k_col_count(CsrView P, int* __restrict__ cnt) {
+  GSTRIDE(i, P.n) for (int k = P.ptr[i]; k < P.ptr[i + 1]; ++k) atomicAdd(cnt + P.col[k], 1);
+}
+__global__ void k_col_scatter(CsrView P, const int* __restrict__ Rptr, int* __restrict__ cur,
+                              int* __restrict__ tcol, double* __restrict__ tval) {
+  GSTRIDE(i, P.n) {
+    for (int k = P.ptr[i]; k < P.ptr[i + 1]; ++k) {
+      const int J = P.col[k];
+      const int pos = Rptr[J] + atomicAdd(cur + J, 1);
+      tcol[pos] = (int)i;
+      tval[pos] = P.val[k];
+    }
+  }
+}
+__global__ void k_row_sort(int rows, const int* __restrict__ ptr, const int* __restrict__ tcol,
+                           const double* __restrict__ tval, int* __restrict__ col,
+                           double* __restrict__ val) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < rows; r += nwarps) {
+    const int b = ptr[r], e = ptr[r + 1];
+    for (int k = b + lane; k < e; k += 32) {
+      const int c = tcol[k];
+      int rank = 0;
+      for (int f = b; f < e; ++f) rank += tcol[f] < c;
+      col[b + rank] = c;
+      val[b + rank] = tval[k];
+    }
+  }
+}
+
 CsrMat transpose(const CsrMat& P, cudaStream_t s) {
+  static const bool sortPath = std::getenv("LDU_AMG_SORT_GEMM") && std::atoi(std::getenv("LDU_AMG_SORT_GEMM")) != 0;
+  if (!sortPath) {
+    Scratch sc(s);
+    const int nr = P.ncols;
+    int* cnt = sc.get<int>(nr + 1);
+    int* cur = sc.get<int>(nr + 1);
+    CUDA_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int) * (nr + 1), s));
+    CUDA_CHECK(cudaMemsetAsync(cur, 0, sizeof(int) * (nr + 1), s));
+    k_col_count<<<nblk(P.nrows), kSB, 0, s>>>(view(P), cnt);
+    CsrMat R;
+    R.nrows = nr;
+    R.ncols = P.nrows;
+    R.nnz = P.nnz;
+    R.ptr = dmalloc<int>(nr + 1);
+    exclusive_scan<int>(cnt, R.ptr, nr, s);
+    int* tcol = sc.get<int>(std::max(1LL, P.nnz));
+    double* tval = sc.get<double>(std::max(1LL, P.nnz));
+    k_col_scatter<<<nblk(P.nrows), kSB, 0, s>>>(view(P), R.ptr, cur, tcol, tval);
+    R.col = dmalloc<int>(P.nnz);
+    R.val = dmalloc<double>(P.nnz);
+    const int grid = (int)std::max(1LL, std::min<long long>(((long long)nr * 32 + kSB - 1) / kSB, 148LL * 64));
+    k_row_sort<<<grid, kSB, 0, s>>>(nr, R.ptr, tcol, tval, R.col, R.val);
+    CUDA_CHECK(cudaGetLastError());
+    R.group = group_of(R.nnz, nr);
+    sub_mark("transpose");
+    return R;
+  }
   Scratch sc(s);
   unsigned long long* key = sc.get<unsigned long long>(P.nnz);
   double* val = sc.get<double>(P.nnz);
   k_expand_T_of<<<nblk(P.nrows), kSB, 0, s>>>(view(P), P.ncols, key, val);
-  return assemble(P.ncols, P.nrows, P.nnz, key, val, false, s);
+  CsrMat R = assemble(P.ncols, P.nrows, P.nnz, key, val, false, s);
+  sub_mark("transpose");
+  return R;
 }
 
 CsrMat galerkin(const CsrMat& A, const CsrMat& P, const CsrMat& R, cudaStream_t s) {
   const int n = A.nrows, nc = P.ncols;
-  CsrMat AP = assemble_rows(
-      n, nc, true, s, [&](long long* cnt) { k_count_AP<<<nblk(n), kSB, 0, s>>>(view(A), P.ptr, cnt); },
-      [&](int r0, int r1, const long long* off, unsigned long long* key, double* val) {
-        k_expand_AP<<<nblk(r1 - r0), kSB, 0, s>>>(view(A), view(P), nc, r0, r1, off, key, val);
-      });
-  try {
-    CsrMat Ac = assemble_rows(
-        nc, nc, true, s,
-        [&](long long* cnt) { k_count_RAP<<<nblk(nc), kSB, 0, s>>>(view(R), AP.ptr, cnt); },
+  CsrMat AP;
+  if (!spgemm_rows(A, BCsr{view(P)}, nc, true, true, AP, s))
+    AP = assemble_rows(
+        n, nc, true, s, [&](long long* cnt) { k_count_AP<<<nblk(n), kSB, 0, s>>>(view(A), P.ptr, cnt); },
         [&](int r0, int r1, const long long* off, unsigned long long* key, double* val) {
-          k_expand_RAP<<<nblk(r1 - r0), kSB, 0, s>>>(view(R), view(AP), nc, r0, r1, off, key, val);
+          k_expand_AP<<<nblk(r1 - r0), kSB, 0, s>>>(view(A), view(P), nc, r0, r1, off, key, val);
         });
+  try {
+    CsrMat Ac;
+    if (!spgemm_rows(R, BCsr{view(AP)}, nc, true, false, Ac, s))
+      Ac = assemble_rows(
+          nc, nc, true, s,
+          [&](long long* cnt) { k_count_RAP<<<nblk(nc), kSB, 0, s>>>(view(R), AP.ptr, cnt); },
+          [&](int r0, int r1, const long long* off, unsigned long long* key, double* val) {
+            k_expand_RAP<<<nblk(r1 - r0), kSB, 0, s>>>(view(R), view(AP), nc, r0, r1, off, key, val);
+          });
     AP.release();
     return Ac;
   } catch (...) {
@@ -1082,7 +1397,10 @@ double* dense_inverse(const CsrMat& A, cudaStream_t s) {
   return I;
 }
 
-// LDU_AMG_TRACE=1: per-phase host wall times of the setup on stderr (stream synchronised)
+// LDU_AMG_TRACE=1: per-phase host wall times of the setup on stderr (stream synchronised);
+// LDU_AMG_TRACE=2 adds the sub-phases of the products (sub_mark)
+struct PhaseTrace;
+PhaseTrace* g_trace = nullptr;
 struct PhaseTrace {
   bool on = false;
   cudaStream_t s = nullptr;
@@ -1104,6 +1422,10 @@ struct PhaseTrace {
     t0 = t;
   }
 };
+void sub_mark(const char* what) {
+  static const bool on = std::getenv("LDU_AMG_TRACE") && std::atoi(std::getenv("LDU_AMG_TRACE")) >= 2;
+  if (on && g_trace) g_trace->mark(what, -1);
+}
 
 void free_level(AmgLevel& L) {
   L.A.release();
@@ -1174,6 +1496,7 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
   try {
     const int hashed = o.keyIndexOrder ? 0 : 1;
     PhaseTrace tr(s);
+    g_trace = &tr;
     CsrMat A = level0_csr(h, s);
     tr.mark("csr0", 0);
     double* diag = h->diag;

@@ -6,7 +6,6 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("LDU_AMG_TRACE", "1")
 import torch  # noqa: E402
 
 import meshgen  # noqa: E402
@@ -16,7 +15,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 s = meshgen.hex_laplacian(n, n, n, dirichlet=dict(x0=1.0))
 A = ldu.LduMatrix.from_system(s)
 b = torch.from_numpy(s.b).cuda()
-for rep in range(3):
+for rep in range(int(os.environ.get('REPS', '3'))):
     t = time.time()
     info = A.amg_setup()
     torch.cuda.synchronize()
