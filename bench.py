@@ -410,7 +410,8 @@ def main():
             # live launch time; the §8(d) LDU-model figure is reported only as the labelled
             # "model-equivalent" rate (it counts int32 addressing and unfused passes the DIA
             # layout and the fused pass never move, so it can exceed the copy peak)
-            roof = {"kernel": kname if solver == "pcg" else ("k_pipe_SU" if fused else "k_pipe_U"),
+            pk = ("k_pipe_SU_mr" if world > 1 else "k_pipe_SU") if fused else "k_pipe_U"
+            roof = {"kernel": kname if solver == "pcg" else pk,
                     "bound": "hbm", "achieved": fb / t_launch / 1e9, "peak": peak, "unit": "GB/s",
                     "frac": fb / t_launch / 1e9 / peak, "traffic": ncu_traffic(solver, n, world),
                     "bytes_per_launch": fb, "launch_us": t_launch * 1e6,
