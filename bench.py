@@ -40,7 +40,8 @@ def parse():
     p.add_argument("--solver", default="pipecg", choices=["pcg", "pipecg"],
                    help="headline solver; the other one is measured too (key 'secondary')")
     p.add_argument("--no-secondary", action="store_true")
-    p.add_argument("--n", type=int, default=256, help="mesh is n^3 (config 3: 256)")
+    p.add_argument("--cube", "--n", dest="n", type=int, default=256,
+                   help="mesh is n^3 (config 3: 256; config 4: 512)")
     p.add_argument("--iters", type=int, default=200, help="fixed CG iterations per step")
     p.add_argument("--batch", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")

@@ -756,7 +756,11 @@ __global__ void k_build_tail_meta(int L, const int* __restrict__ tailIf, const i
   }
 }
 
-template <class Fmt, int R, int MINB = 5>
+// FOLD = true (default loop): no separate control kernel.  The pass launches the next pass
+// programmatically as soon as it starts (that pass's blocks take the SMs this one frees and wait
+// in griddepcontrol.wait), and its last block, after publishing the sums, gathers every rank's
+// sums from its own mailbox and runs the control step of the next iteration itself.
+template <class Fmt, int R, int MINB = 5, bool FOLD = false>
 __global__ void __launch_bounds__(kBlock, MINB) k_pipe_SU_mr(Fmt A, const double* __restrict__ rD,
                                                        double* w0, double* w1,
                                                        double* __restrict__ z,
@@ -789,6 +793,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_pipe_SU_mr(Fmt A, const double
   }
   pdl_wait();  // the control step has finished: alpha_i, beta_i, done
   if (st->done) return;
+  if (FOLD) pdl_trigger();
   const int k = st->k;
   if (tid == 0) tstamp(d, k, 2, 1);
   const PipeRow P{st->pa, st->pb, st->norm == LDU_NORM_L2};
@@ -872,6 +877,27 @@ __global__ void __launch_bounds__(kBlock, MINB) k_pipe_SU_mr(Fmt A, const double
     d->seqHaloSend = seqOut;
     d->snapK = k;
     tstamp(d, k, 13, 0);
+  }
+  if (FOLD) {  // the control step of iteration k + 1, in this block
+    __shared__ double part[kP2PMaxRanks][3];
+    char* me = d->base[d->rank];
+    for (int q = tid; q < d->nRanks; q += blockDim.x) {
+      const uint64_t* src = mb_redll(me, (int)(sq & 1), q);
+#pragma unroll
+      for (int m = 0; m < 3; ++m) part[q][m] = ll_load(src + 2 * m, (uint32_t)sq);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double sums[kMaxVals] = {0.0, 0.0, 0.0, 0.0};
+      for (int q = 0; q < d->nRanks; ++q)
+        for (int m = 0; m < 3; ++m) sums[m] += part[q][m];
+      d->seqRed = sq;
+      if (d->nIf > 0) d->seqHalo += 1;  // exchange k, read by this pass (every block is done)
+      run_ctl(CTL_PIPE_NEXT, st, sums);
+      if (d->nIf > 0 && st->done) d->seqHalo += 1;  // exchange k + 1, sent here, never read
+      tstamp(d, k + 1, 0, 0);
+      tstamp(d, k + 1, 1, 0);
+    }
   }
 }
 
@@ -1486,6 +1512,28 @@ long long enqueue_pipe_iters(ldu_handle h, int batch, cudaStream_t s, bool profi
     MrTail T{h->mrGapStart, haveIf ? h->mrGapLen : h->n, h->mrTailMeta, h->ifCellPtr, h->ifFaceIdx,
              h->ifCoeffs, h->ifFaceIf, h->nIfFaces};
     const bool pdl = h->pdl && h->trace.empty();
+    if (h->mrFold && !rrFirst) {  // one kernel per iteration, control step in its last block
+      for (int it = 0; it < batch; ++it) {
+        trace_mark(h, it, 0, s);
+        trace_mark(h, it, 1, s);
+        prof_mark(h, profile, 4 * it + 0, s);
+        prof_mark(h, profile, 4 * it + 1, s);
+        prof_mark(h, profile, 4 * it + 2, s);
+        Red ru = red_loop(h, CTL_NONE, false, h->gridSUmr);
+        with_format(h, [&](auto A) {
+          using Fmt = decltype(A);
+          launch_pdl(pdl && it > 0 && !profile, k_pipe_SU_mr<Fmt, 0, 5, true>, h->gridSUmr, kBlock, s,
+                     A, (const double*)h->rD, h->w, h->w2, h->z, h->s, h->p0, h->x, h->r, h->st,
+                     ru, T, h->p2pDesc);
+        });
+        ++kernels;
+        prof_mark(h, profile, 4 * it + 3, s);
+        trace_mark(h, it, 2, s);
+        trace_mark(h, it, 3, s);
+        trace_mark(h, it, 4, s);
+      }
+      return kernels;
+    }
     for (int it = 0; it < batch; ++it) {
       trace_mark(h, it, 0, s);
       launch_pdl(pdl && it > 0 && !profile, k_ctl_ll, 1, 64, s, h->st, h->p2pDesc,
@@ -1960,6 +2008,10 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
     if (h->p2pOn && h->fusePipe && h->mrFuse) {
       k_mr_init<<<1, 32, 0, s>>>(h->p2pDesc, h->st);
       ++kernels;
+      if (h->mrFold && !rr) {  // the folded loop starts at iteration 0 with alpha_0 known
+        k_ctl_ll<<<1, 64, 0, s>>>(h->st, h->p2pDesc, 1);
+        ++kernels;
+      }
     }
   }
   CUDA_CHECK(cudaEventRecord(h->ev[1], s));
@@ -2085,7 +2137,8 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   std::vector<float> traceT;  // LDU_TRACE: [batch][it < batch-1][5]
   // multi-rank pipelined needs one more loop trip: the decision on r_i is taken by the
   // control kernel after the overlapped allgather of trip i (single rank: in U_{i-1}).
-  const long long trips = (long long)maxIter + ((pipelined && mr) ? 1 : 0);
+  const bool folded = pipelined && mr && h->p2pOn && h->fusePipe && h->mrFuse && h->mrFold && !rr;
+  const long long trips = (long long)maxIter + ((pipelined && mr && !folded) ? 1 : 0);
   auto collect = [&]() {
     for (int it = 0; it < batch; ++it)
       for (int p = 0; p < 2; ++p) {
@@ -2217,7 +2270,7 @@ ldu_status solve(ldu_handle h, bool pipelined, const double* b, double* x, doubl
   h->stats.reductions = sh->nRed;                      // counted on the device (run_ctl)
   h->stats.allreduces = mr ? (long long)sh->nRed : 0;  // every multi-rank control step gathers
   if (profile) {  // passes that did work: trips 0 .. iter-1 (multi-rank pipelined: 1 .. iter)
-    const long long first = (pipelined && mr) ? 1 : 0;
+    const long long first = (pipelined && mr && !folded) ? 1 : 0;
     for (long long g = first; g < first + sh->iter && g < (long long)passT.size() / 2; ++g)
       for (int p = 0; p < 2; ++p) {
         h->stats.passMs[p] += passT[2 * g + p];
@@ -2414,6 +2467,8 @@ void configure(ldu_handle h) {
   if (const char* v = std::getenv("LDU_PDL")) h->pdl = std::atoi(v) != 0;
   h->mrFuse = true;
   if (const char* v = std::getenv("LDU_MR_FUSE")) h->mrFuse = std::atoi(v) != 0;
+  h->mrFold = true;
+  if (const char* v = std::getenv("LDU_MR_FOLD")) h->mrFold = std::atoi(v) != 0;
   h->mrPre = 4;
   if (const char* v = std::getenv("LDU_MR_PRE")) h->mrPre = std::atoi(v) >= 8 ? 8 : (std::atoi(v) >= 4 ? 4 : 0);
   // persistent cooperative kernels for single-rank, latency-bound sizes (LDU_PERSIST=0/1 forces)
