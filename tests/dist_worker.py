@@ -134,7 +134,8 @@ def main():
             sto, ito, reso = fn(b, xo, tol=1e-6, maxIter=5000, norm=ldu.NORM_OPENFOAM,
                                 relTol=0.01, minIter=3, record_history=True)
             out[solver + "_of"] = (sto, ito, reso, xo.cpu().numpy(), A.history())
-            if solver == "pipecg" and os.environ.get("LDU_PIPE_FUSE", "1") != "0":
+            if (solver == "pipecg" and os.environ.get("LDU_PIPE_FUSE", "1") != "0"
+                    and os.environ.get("LDU_P2P", "1") != "0"):
                 # residual replacement every 25 iterations across ranks (NEXT-4, reading Z7)
                 xr = torch.zeros_like(b)
                 str_, itr, resr = fn(b, xr, tol=1e-10, maxIter=5000, replaceEvery=25,
