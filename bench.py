@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--no-profile", action="store_true", help="skip per-pass event timing")
     p.add_argument("--no-amg", action="store_true", help="skip the AMG-PCG time-to-solution leg")
     p.add_argument("--amg-tol", type=float, default=1e-8)
+    p.add_argument("--no-c5", action="store_true",
+                   help="skip the c5 irregular (SELL-32) evidence leg")
+    p.add_argument("--c5-n", type=int, default=160, help="c5 leg: irregular mesh base n^3")
     return p.parse_args()
 
 
@@ -478,6 +481,8 @@ def main():
     amg = None
     if world == 1 and not args.no_amg:
         ai = A.amg_setup()
+        setup_cold = ai["setupMs"]
+        ai = A.amg_setup()  # again: the first build in a process also pays the allocator's first touch
         tol = args.amg_tol
         for _ in range(2):
             x.zero_()
@@ -518,6 +523,7 @@ def main():
                "operator_complexity": ai["operatorComplexity"],
                "jacobi_pcg": {"iterations": jit, "ms_per_solve": 1e3 * t_jac, "status": int(jst)},
                "time_to_solution_speedup_vs_jacobi_pcg": t_jac / t_amg,
+               "setup_ms_first_in_process": setup_cold,
                "setup_plus_solve_ms": ai["setupMs"] + 1e3 * t_amg,
                "speedup_vs_jacobi_pcg_incl_setup": t_jac / (t_amg + ai["setupMs"] / 1e3),
                "gpu_launches_per_solve": akern // args.steps,
@@ -525,6 +531,45 @@ def main():
                           "achieved": vb / (vc_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                           "frac": vb / (vc_ms / 1e3) / 1e9 / peak, "bound": "hbm",
                           "peak_source": peak_src}}
+
+    # c5 evidence leg (SURVEY §8(d) config 5 recipe at a reduced base size, 1 GPU): the irregular
+    # RCM mesh on the SELL-32 layout, fixed iterations, live per-launch time of the fused pass
+    # against the bytes the SELL-32 layout must move (12 B per stored entry incl. padding)
+    c5 = None
+    if world == 1 and not args.no_c5:
+        g5 = meshgen.irregular_mesh(args.c5_n, seed=1505)
+        A5 = ldu.LduMatrix.from_system(g5)
+        A5.set_stream(stream.cuda_stream)
+        i5 = A5.info()
+        b5 = torch.from_numpy(g5.b).cuda()
+        x5 = torch.zeros_like(b5)
+        c5 = {"workload": f"c5 recipe, irregular {args.c5_n}^3 base ({g5.nCells:,} cells, "
+                          f"{g5.nFaces:,} faces), RCM order", "layout": i5["layout_name"],
+              "stored_entries_per_row": i5["storedEntries"] / g5.nCells}
+        for solver in ("pipecg", "pcg"):
+            fn5 = A5.pcg_solve if solver == "pcg" else A5.pipecg_solve
+            for _ in range(2):
+                x5.zero_()
+                fn5(b5, x5, tol=0.0, maxIter=args.iters)
+            barrier()
+            c0 = torch.cuda.Event(enable_timing=True)
+            c1 = torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            for _ in range(3):
+                x5.zero_()
+                fn5(b5, x5, tol=0.0, maxIter=args.iters)
+            c1.record(stream)
+            barrier()
+            rate = 3 * args.iters / (c0.elapsed_time(c1) / 1e3)
+            x5.zero_()
+            fn5(b5, x5, tol=0.0, maxIter=args.iters, profile=True)
+            s5 = A5.stats()
+            slot = 1 if solver == "pipecg" else 0
+            us = s5["passMs"][slot] / max(1, s5["passLaunches"][slot]) * 1e3
+            fb5 = pass_format_bytes(solver, i5, g5.nCells)
+            c5[solver] = {"iter_per_s": rate, "pass_us": us, "pass_bytes": fb5,
+                          "pass_gbps": fb5 / us / 1e3, "pass_frac": fb5 / us / 1e3 / peak}
+        A5.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -549,7 +594,7 @@ def main():
                "model_bytes_per_iter": bytes_iter, "model_equivalent_gbps": main_r["model_eff"],
                "stream_triad_gbps": triad, "hbm_peak_gbps": peak, "hbm_peak_source": peak_src,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": kernels,
-               "secondary": secondary, "amg": amg,
+               "secondary": secondary, "amg": amg, "c5_irregular": c5,
                "clocks": clk, "last_status": int(st), "iterations_per_step": it}
         print(json.dumps(out), flush=True)
     A.close()

@@ -633,6 +633,23 @@ __global__ void k_lz_matvec(CsrView A, const double* __restrict__ sd, const doub
   block_store<1>(a, part);
 }
 
+// the same on the handle's own layout (level 0: DIA / SELL rows, coalesced, diagonal first)
+template <class Fmt>
+__global__ void k_lz_matvec_fmt(Fmt A, const double* __restrict__ diag, const double* __restrict__ sd,
+                                const double* __restrict__ v, const double* __restrict__ vprev,
+                                const double* __restrict__ beta, double* __restrict__ w, double* part) {
+  const double b = *beta;
+  double a[1] = {0.0};
+  GSTRIDE(i, A.n) {
+    double acc = diag[i] * (sd[i] * v[i]);
+    for_row(A, (int)i, [&](int j, double aij) { acc += aij * (sd[j] * v[j]); });
+    const double wi = sd[i] * acc - b * vprev[i];
+    w[i] = wi;
+    a[0] += wi * v[i];
+  }
+  block_store<1>(a, part);
+}
+
 // w -= alpha v; partial (w, w)
 __global__ void k_lz_orth(int n, double* __restrict__ w, const double* __restrict__ v,
                           const double* __restrict__ alpha, double* part) {
@@ -695,7 +712,7 @@ __global__ void k_tridiag_max(int m, const double* __restrict__ al, const double
 }
 
 double lanczos_omega(const CsrMat& A, const double* diag, int steps, cudaStream_t s,
-                     double* ritzOut) {
+                     double* ritzOut, ldu_handle h0 = nullptr) {
   Scratch sc(s);
   const int n = A.nrows;
   const int G = nblk(n);
@@ -715,7 +732,12 @@ double lanczos_omega(const CsrMat& A, const double* diag, int steps, cudaStream_
   CUDA_CHECK(cudaMemsetAsync(scal + 1, 0, sizeof(double), s));
   int m = 0;
   for (int j = 0; j < ms; ++j) {
-    k_lz_matvec<<<G, kSB, 0, s>>>(view(A), sd, v, vp, scal + 1, w, part);
+    if (h0)  // level 0: the handle's layout instead of the assembled CSR (same operator)
+      with_layout(h0, [&](auto L) {
+        k_lz_matvec_fmt<<<G, kSB, 0, s>>>(L, diag, sd, v, vp, scal + 1, w, part);
+      });
+    else
+      k_lz_matvec<<<G, kSB, 0, s>>>(view(A), sd, v, vp, scal + 1, w, part);
     k_sum_parts<<<1, kSB, 0, s>>>(part, G, al + j);
     k_lz_orth<<<G, kSB, 0, s>>>(n, w, v, al + j, part);
     k_sum_parts<<<1, kSB, 0, s>>>(part, G, be + j);
@@ -1519,7 +1541,7 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
       L.rD = rD;
       L.ownsDiag = owns;
       L.agg = agg;
-      L.omega = lanczos_omega(A, diag, o.lanczosSteps, s, nullptr);
+      L.omega = lanczos_omega(A, diag, o.lanczosSteps, s, nullptr, H->lv.empty() ? h : nullptr);
       tr.mark("lanczos", (int)H->lv.size());
       L.P = build_P(A, agg, nAgg, diag, L.omega, !o.unsmoothed, s);
       L.R = transpose(L.P, s);
