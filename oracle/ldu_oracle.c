@@ -338,7 +338,8 @@ int oracle_pipecg_rr(int n, int nf, const int *l, const int *u, const double *di
  * aggregation-based AMG with weighted Jacobi iterations with omega = 4/3 as a smoother", the
  * aggregates coming from "the parallel aggregation method based on a distance-2
  * maximal-independent-set".  Readings Z27-Z33 fix what the paper leaves open:
- * smoothed aggregation P = (I - w D^-1 A) T with w = (4/3)/rho, rho = max_i sum_j |A_ij| / A_ii;
+ * smoothed aggregation P = (I - w D^-1 A) T with w = (4/3)/rho, rho = 1.05 x the largest Ritz
+ * value of 20 Lanczos steps on D^-1/2 A D^-1/2 (oracle/amg.py spectral_radius; reading Z27);
  * all couplings strong; one pre- and one post-sweep of w-Jacobi from a zero guess; MIS-2 in the
  * priority order key(i) below; Galerkin A_c = P^T A P; coarsest level solved exactly (Cholesky).
  * The hierarchy products are built by oracle/amg.py (scipy); this file holds the integer
