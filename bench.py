@@ -314,15 +314,24 @@ def main():
     import meshgen
     import paper_1505_07630_b200 as ldu
 
+    # LDU_DIST_BOOT=host: gloo + ldu_comm_init_host (no NCCL; ranks may share GPUs -- used to
+    # exercise more ranks than the box has GPUs; timings are then not a scaling measurement)
+    host_boot = os.environ.get("LDU_DIST_BOOT", "nccl") == "host" and world > 1
+    if host_boot:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     comm = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        uid = [ldu.Comm.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = ldu.Comm(rank, world, uid[0], local)
+        if host_boot:
+            dist.init_process_group("gloo")
+            comm = ldu.Comm.host(rank, world, local)
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            uid = [ldu.Comm.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = ldu.Comm(rank, world, uid[0], local)
 
     n = args.n
     if world == 1:
@@ -344,10 +353,20 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def allreduce_(t, op=None):
+        """in-place all-reduce of a small CUDA tensor (through the host under gloo)"""
+        kw = {} if op is None else {"op": op}
+        if host_boot:
+            c = t.cpu()
+            dist.all_reduce(c, **kw)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t, **kw)
+
     # global byte model
     tot = torch.tensor([N, F, P], dtype=torch.float64, device="cuda")
     if dist is not None:
-        dist.all_reduce(tot)
+        allreduce_(tot)
     Ng, Fg, Pg = (float(v) for v in tot.tolist())
     peak, peak_src = hbm_peak()
     # the paper's STREAM-measured roofline (P:44, P:49): our fp64 triad, same run, same device
@@ -398,7 +417,7 @@ def main():
         clk = clocks.stop() if clocks else None
         t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
         if dist is not None:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            allreduce_(t, dist.ReduceOp.MAX)
         elapsed = float(t.item())
         value = args.steps * args.iters / elapsed
         # roofline of the dominant kernel (this rank), timed live with CUDA event nodes
@@ -428,7 +447,7 @@ def main():
         fb_iter = torch.tensor([float(iter_format_bytes(solver, info, N, P))], dtype=torch.float64,
                                device="cuda")
         if dist is not None:
-            dist.all_reduce(fb_iter)
+            allreduce_(fb_iter)
         fb_iter = float(fb_iter.item())
         return dict(value=value, elapsed=elapsed, kernels=kernels, roof=roof, clk=clk,
                     status=int(st), iters=it, bytes_iter=bytes_iter, fb_iter=fb_iter,
@@ -473,7 +492,7 @@ def main():
         barrier()
         te = torch.tensor([f0.elapsed_time(f1) / 1e3], dtype=torch.float64, device="cuda")
         if dist is not None:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            allreduce_(te, dist.ReduceOp.MAX)
         e2e = {"value": args.steps * args.iters / float(te.item()), "unit": UNIT,
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
 
