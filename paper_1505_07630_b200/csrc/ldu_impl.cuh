@@ -220,6 +220,7 @@ struct ldu_handle_s {
   int gridSUmr = 0, mrPre = 4;           // grid / pre-phase rows per thread (LDU_MR_PRE: 0, 4, 8)
   bool mrFuse = true;                    // one kernel per iteration (LDU_MR_FUSE=0: pack + fix-up)
   bool mrFold = true;                    // ... with the control step in its last block (LDU_MR_FOLD)
+  bool cgLL = true;                      // classical multi-rank: LL reductions (LDU_CG_LL)
   unsigned long long* tbuf = nullptr;    // LDU_TRACE device timestamps
 };
 

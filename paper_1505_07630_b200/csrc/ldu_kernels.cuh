@@ -328,7 +328,44 @@ struct Red {  // reduction plumbing of one pass
   int total;       // slots summed by the last block
   int store_only;  // 1: store partials only (a later kernel finishes the reduction)
   P2PDesc* p2p;    // multi-rank over peer memory: publish the local sums to every rank
+  int llctl;       // != 0 (multi-rank, peer memory): publish the sums as LL words, gather every
+                   // rank's in the same last block and run this control step there (no flag, no
+                   // fence, no control kernel)
+  int llHalo;      // halo exchanges consumed by this pass (retired by that control step)
 };
+
+// Last block of an LL-reducing pass: the sums (NV <= 4) to every rank's mailbox as LL words
+// (lane q -> rank q), every rank's sums back from this rank's mailbox, summed in rank order,
+// the control step.  Out of line: the streaming loops of the kernels that inline
+// finish_reduction keep their registers.
+template <int NV>
+__device__ __noinline__ void ll_reduce_ctl(const Red& rd, State* st) {
+  P2PDesc* d = rd.p2p;
+  __shared__ double part[kP2PMaxRanks][NV];
+  const unsigned long long sq = d->seqRed + 1;
+  const int par = (int)(sq & 1);
+  __syncthreads();
+  for (int q = threadIdx.x; q < d->nRanks; q += blockDim.x) {
+    uint64_t* dst = mb_redll(d->base[q], par, d->rank);
+#pragma unroll
+    for (int m = 0; m < NV; ++m) ll_store(dst + 2 * m, __ldcg(rd.sums + m), (uint32_t)sq);
+  }
+  char* me = d->base[d->rank];
+  for (int q = threadIdx.x; q < d->nRanks; q += blockDim.x) {
+    const uint64_t* src = mb_redll(me, par, q);
+#pragma unroll
+    for (int m = 0; m < NV; ++m) part[q][m] = ll_load(src + 2 * m, (uint32_t)sq);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sums[kMaxVals] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = 0; q < d->nRanks; ++q)
+      for (int m = 0; m < NV; ++m) sums[m] += part[q][m];
+    d->seqRed = sq;
+    d->seqHalo += rd.llHalo;
+    run_ctl(rd.llctl, st, sums);
+  }
+}
 
 template <int NV>
 __device__ __forceinline__ void finish_reduction(double (&v)[NV], const Red& rd, State* st) {
@@ -348,6 +385,17 @@ __device__ __forceinline__ void finish_reduction(double (&v)[NV], const Red& rd,
     if (threadIdx.x == 0 && rd.ctl != CTL_NONE) run_ctl(rd.ctl, st, rd.sums);
     if (threadIdx.x == 0 && rd.p2p) p2p_publish_sums<NV>(rd.p2p, rd.sums);
     if (threadIdx.x == 0) tstamp(rd.p2p, st->k, 10, 0);
+  }
+}
+
+// finish_reduction for the LL multi-rank passes (classical CG's fix-up and pass B): only those
+// kernels instantiate it, so the single-rank passes keep their register allocation
+template <int NV>
+__device__ __forceinline__ void finish_reduction_ll(double (&v)[NV], const Red& rd, State* st) {
+  if (store_partial_is_last<NV>(v, rd.partials, rd.ld, rd.slot_base + blockIdx.x, rd.ticket,
+                                gridDim.x)) {
+    sum_partials<NV>(rd.partials, rd.ld, rd.total, rd.sums, rd.ticket);
+    ll_reduce_ctl<NV>(rd, st);
   }
 }
 

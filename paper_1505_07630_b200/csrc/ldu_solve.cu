@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_passA_dia(DiaView<ND> A,
 }
 
 // classical pass B_k
+template <bool LL = false>  // LL: multi-rank, the reduction and control B in the last block
 __global__ void __launch_bounds__(kBlock) k_cg_passB(int n, const double* __restrict__ rD,
                                                      const double* __restrict__ q,
                                                      double* __restrict__ r, State* st, Red rd) {
@@ -370,7 +371,8 @@ __global__ void __launch_bounds__(kBlock) k_cg_passB(int n, const double* __rest
     v[0] = fma(rc, rD[c] * rc, v[0]);
     v[1] += l2 ? rc * rc : fabs(rc);
   }
-  finish_reduction<2>(v, rd, st);
+  if (LL) finish_reduction_ll<2>(v, rd, st);
+  else finish_reduction<2>(v, rd, st);
 }
 
 // classical exit: x += alpha_k p_k if pending
@@ -590,7 +592,8 @@ __global__ void __launch_bounds__(kBlock) k_iface_cg_p2p(int nIfCells, const int
     q[c] -= corr;
     v[0] -= pnew[c] * corr;
   }
-  finish_reduction<1>(v, rd, st);
+  if (rd.llctl) finish_reduction_ll<1>(v, rd, st);
+  else finish_reduction<1>(v, rd, st);
 }
 
 // Multi-rank fused pipelined pass, fix-up of the interface rows once the halo has arrived:
@@ -1282,6 +1285,8 @@ Red red_of(ldu_handle h, int ctl, bool single, int grid = 0) {
   r.total = grid ? grid : h->grid;
   r.store_only = 0;
   r.p2p = nullptr;
+  r.llctl = 0;
+  r.llHalo = 0;
   return r;
 }
 
@@ -1453,17 +1458,33 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
         const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->gridA);
         ri.slot_base = h->gridA;
         ri.total = h->gridA + ig;
+        if (h->cgLL) {  // (p, q) as LL words; control A in the fix-up's last block
+          ri.llctl = CTL_CG_A;
+          ri.llHalo = 1;
+        }
         k_iface_cg_p2p<<<ig, kBlock, 0, s>>>(h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx,
                                              h->ifCoeffs, h->q, h->p0, h->p1, h->st, ri,
                                              h->p2pDesc, h->nIfFaces);
         ++kernels;
       }
-      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_CG_A, h->st, h->p2pDesc, haveIf ? 1 : 0);
+      if (!(h->cgLL && haveIf)) {
+        k_ctl_p2p<<<1, 32, 0, s>>>(CTL_CG_A, h->st, h->p2pDesc, haveIf ? 1 : 0);
+        ++kernels;
+      }
       prof_mark(h, profile, 4 * it + 2, s);
-      k_cg_passB<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->q, h->r, h->st, red_loop(h, CTL_CG_B, false));
+      Red rb = red_loop(h, CTL_CG_B, false);
+      if (h->cgLL) {
+        rb.llctl = CTL_CG_B;
+        k_cg_passB<true><<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->q, h->r, h->st, rb);
+      } else {
+        k_cg_passB<false><<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->q, h->r, h->st, rb);
+      }
       prof_mark(h, profile, 4 * it + 3, s);
-      k_ctl_p2p<<<1, 32, 0, s>>>(CTL_CG_B, h->st, h->p2pDesc, 0);
-      kernels += 3;
+      ++kernels;
+      if (!h->cgLL) {
+        k_ctl_p2p<<<1, 32, 0, s>>>(CTL_CG_B, h->st, h->p2pDesc, 0);
+        ++kernels;
+      }
     }
     return kernels;
   }
@@ -1495,7 +1516,7 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
     if (mr) allgather_ctl(h, CTL_CG_A, 1, s, kernels);
     // pass B
     prof_mark(h, profile, 4 * it + 2, s);
-    k_cg_passB<<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->q, h->r, h->st, red_of(h, CTL_CG_B, !mr));
+    k_cg_passB<false><<<h->grid, kBlock, 0, s>>>(h->n, h->rD, h->q, h->r, h->st, red_of(h, CTL_CG_B, !mr));
     prof_mark(h, profile, 4 * it + 3, s);
     ++kernels;
     if (mr) allgather_ctl(h, CTL_CG_B, 2, s, kernels);
@@ -2469,6 +2490,8 @@ void configure(ldu_handle h) {
   if (const char* v = std::getenv("LDU_MR_FUSE")) h->mrFuse = std::atoi(v) != 0;
   h->mrFold = true;
   if (const char* v = std::getenv("LDU_MR_FOLD")) h->mrFold = std::atoi(v) != 0;
+  h->cgLL = true;  // classical multi-rank: LL reductions, control steps in the last blocks
+  if (const char* v = std::getenv("LDU_CG_LL")) h->cgLL = std::atoi(v) != 0;
   h->mrPre = 4;
   if (const char* v = std::getenv("LDU_MR_PRE")) h->mrPre = std::atoi(v) >= 8 ? 8 : (std::atoi(v) >= 4 ? 4 : 0);
   // persistent cooperative kernels for single-rank, latency-bound sizes (LDU_PERSIST=0/1 forces)
@@ -2491,7 +2514,7 @@ void configure(ldu_handle h) {
     long long g = (long long)sms * std::max(1, o);
     return (int)std::max(1LL, std::min(g, need));
   };
-  h->grid = grid_of((const void*)k_cg_passB);  // streaming passes
+  h->grid = grid_of((const void*)k_cg_passB<false>);  // streaming passes
   // plane-marching geometry (DIA with one far offset D >= 4096 and near offsets <= 1024)
   h->marchOk = false;
   if (h->layout == LDU_LAYOUT_DIA_SYM && h->nd >= 2) {
