@@ -121,3 +121,27 @@ def test_cavity_piso_sequence_512(ldu, solver, norm):
     if norm == "L2":
         r = b - oracle.amul(s, xg)
         assert np.linalg.norm(r) / np.linalg.norm(b) <= 10 * 1e-6
+
+
+@pytest.mark.parametrize("solver", ["pcg", "pipecg"])
+def test_cavity_1024_fixed_iterations(ldu, solver):
+    """Config 2 at its full size (1024^2 cavity, OpenFOAM criterion): 60 fixed iterations from a
+    warm start, in the launch configuration the library picks there (the persistent cooperative
+    kernels: the working set fits in L2), against the oracle's 60 (a full solve takes the oracle
+    ~2 min: 5648 iterations)."""
+    nx = 1024
+    s = meshgen.cavity_pressure_2d(nx, nx)
+    b = meshgen.cavity_rhs(nx, nx, 4)
+    x0 = np.random.default_rng(9).uniform(-1, 1, s.nCells)
+    ofn = oracle.pcg if solver == "pcg" else oracle.pipecg
+    ost, ox, oit, ores, ohist = ofn(s, b, x0=x0, tol=0.0, maxIter=60, norm=oracle.NORM_OPENFOAM,
+                                    history=True)
+    with ldu.LduMatrix.from_system(s) as A:
+        fn = A.pcg_solve if solver == "pcg" else A.pipecg_solve
+        x = cuda(x0)
+        st, it, res = fn(cuda(b), x, tol=0.0, maxIter=60, norm=ldu.NORM_OPENFOAM,
+                         record_history=True)
+        hist = A.history()
+    assert st == ldu.NOT_CONVERGED == ost and it == oit == 60
+    assert rel(x.cpu().numpy(), ox) <= 1e-10
+    np.testing.assert_allclose(hist, ohist, rtol=1e-9)
