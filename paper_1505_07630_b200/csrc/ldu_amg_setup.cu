@@ -1161,24 +1161,31 @@ template <class B, int CAP, int G>
 bool spgemm_rows_cap(const CsrMat& A, B b, int ncols, bool drop, CsrMat& C, cudaStream_t s) {
   Scratch sc(s);
   const int n = A.nrows;
-  long long* ub = sc.get<long long>(n + 1);
-  long long* toff = sc.get<long long>(n + 1);
-  k_expansion_bound<<<nblk(n), kSB, 0, s>>>(view(A), b, CAP, ub);
-  exclusive_scan<long long>(ub, toff, n, s);
-  const long long tot = d2h(toff + n, s);
-  int* tcol = sc.get<int>(std::max(1LL, tot));
-  double* tval = sc.get<double>(std::max(1LL, tot));
+  // measured at 256^3: narrow rows (A T, A P) are cheaper counted then written in place (a
+  // bound-spaced scratch scatters their few entries widely); wide rows (R (A P)) in one pass
+  static const bool twoPass = std::getenv("LDU_AMG_GEMM_2PASS") && std::atoi(std::getenv("LDU_AMG_GEMM_2PASS")) != 0;
+  bool onePass = G == 32 && !twoPass;
+  long long* toff = nullptr;
+  int* toff32 = nullptr;
+  int* tcol = nullptr;
+  double* tval = nullptr;
+  if (onePass) {
+    long long* ub = sc.get<long long>(n + 1);
+    toff = sc.get<long long>(n + 1);
+    k_expansion_bound<<<nblk(n), kSB, 0, s>>>(view(A), b, CAP, ub);
+    exclusive_scan<long long>(ub, toff, n, s);
+    const long long tot = d2h(toff + n, s);
+    onePass = tot < (1LL << 31) - 1;  // the kernel writes at int offsets
+    if (onePass) {
+      tcol = sc.get<int>(std::max(1LL, tot));
+      tval = sc.get<double>(std::max(1LL, tot));
+      toff32 = sc.get<int>(n + 1);
+      k_l2i<<<nblk(n + 1), kSB, 0, s>>>(n + 1, toff, toff32);
+    }
+  }
   int* cnt = sc.get<int>(n + 1);
   int* ovf = sc.get<int>(1);
   CUDA_CHECK(cudaMemsetAsync(ovf, 0, sizeof(int), s));
-  // the kernel writes at int offsets: scratch offsets beyond 2^31 take the two-pass route below
-  static const bool twoPass = std::getenv("LDU_AMG_GEMM_2PASS") && std::atoi(std::getenv("LDU_AMG_GEMM_2PASS")) != 0;
-  const bool onePass = tot < (1LL << 31) - 1 && !twoPass;
-  int* toff32 = nullptr;
-  if (onePass) {
-    toff32 = sc.get<int>(n + 1);
-    k_l2i<<<nblk(n + 1), kSB, 0, s>>>(n + 1, toff, toff32);
-  }
   constexpr int rpb = kGemmWarps * (32 / G);
   const int grid = (int)std::max(1LL, std::min<long long>((n + rpb - 1) / rpb, 148LL * 16));
   if (onePass)
