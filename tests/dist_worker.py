@@ -20,6 +20,16 @@ import torch.distributed as dist  # noqa: E402
 import meshgen  # noqa: E402
 
 
+def decoupled_boxes():
+    a = meshgen.hex_laplacian(12, 10, 16, dirichlet=dict(x0=1.0))
+    b = meshgen.hex_laplacian(12, 10, 16, conductance_sigma=0.5, seed=4, dirichlet=dict(x0=2.0))
+    n = a.nCells
+    return meshgen.LduSystem(2 * n, np.concatenate([a.lowerAddr, b.lowerAddr + n]).astype(np.int32),
+                             np.concatenate([a.upperAddr, b.upperAddr + n]).astype(np.int32),
+                             np.concatenate([a.diag, b.diag]), np.concatenate([a.upper, b.upper]),
+                             None, np.concatenate([a.b, b.b]))
+
+
 def slab_bounds_for(g, world):
     """LDU_DIST_BOUNDS: equal (default) cell slabs, Eq 5-8 weighted slabs (work
     fractions proportional to 1, 2, .., world -- a heterogeneous set of speeds), or slabs with
@@ -99,6 +109,9 @@ def main():
         "hex_sigma": lambda: meshgen.hex_laplacian(17, 13, 19, conductance_sigma=0.8, seed=3,
                                                    dirichlet=dict(x0=1.0)),
         "irregular": lambda: meshgen.irregular_mesh(14, seed=7),
+        # two disconnected boxes: with 2 ranks each rank owns one and has NO interface (a rank
+        # of a multi-rank comm with nothing to exchange); with 4 ranks each box is cut once
+        "decoupled": lambda: decoupled_boxes(),
     }
     ok = True
     for name, mk in cases.items():
