@@ -77,7 +77,7 @@ def test_distributed_dic_parity(nproc):
 # ---- ranks sharing the box's GPU(s): host bootstrap, peer-memory path only ------------------
 
 @pytest.mark.parametrize("mode,nproc", [("p2p_fused", 2), ("p2p_split", 2), ("p2p_fused", 4),
-                                        ("p2p_split", 4), ("p2p_fused", 8)])
+                                        ("p2p_fused", 8)])
 def test_distributed_parity_shared_gpu(nproc, mode):
     """SpMV, PCG, PipeCG (fused and split passes), OpenFOAM norm / relTol / minIter and the
     device-counted reductions (1 + 2 it classical, 2 + it pipelined) across nproc ranks."""
