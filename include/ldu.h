@@ -145,8 +145,11 @@ ldu_status pcg_solve(ldu_handle h, const double *b, double *x, double tol, int m
 /* Ghysels-Vanroose pipelined CG with M = diag(A) ("only one collective communication per
  * loop body ... overlapped by the sparse matrix-vector multiplication"; SURVEY
  * §8(c) c3 Jacobi-specialised form): ONE fused reduction of (gamma, delta, ||r||^2) per
- * iteration, overlapped with the SpMV and its halo exchange.  Same arguments and semantics as
- * pcg_solve; the convergence test uses r_i at the top of iteration i (reading Z3). */
+ * iteration.  Across ranks (peer-memory path) each iteration is ONE kernel: the SpMV with its
+ * interface term, the recurrences, the next halo and the rank's share of the reduction written
+ * into the peers' memory over NVLink (LL words), the control step in its last block.  Same
+ * arguments and semantics as pcg_solve; the convergence test uses r_i at the top of iteration i
+ * (reading Z3). */
 ldu_status pipecg_solve(ldu_handle h, const double *b, double *x, double tol, int maxIter,
                         int *nIter, double *finalRes);
 
@@ -163,7 +166,8 @@ typedef struct {
                         (maxIter still ends the solve, NOT_CONVERGED; reading Z26)            */
   int replaceEvery;  /* pipelined CG only (NEXT-4): > 0 recomputes r = b - A x, w = A M r, s = A p,
                         z = A M s from their definitions after every replaceEvery-th iteration
-                        (residual replacement, attainable accuracy); 0 = off.  Single rank.    */
+                        (residual replacement, attainable accuracy); 0 = off.  Single rank, and
+                        across ranks on the peer-memory path (not with the NCCL fallback).   */
   double relTol;     /* OpenFOAM relTol: also converged when res < relTol * res0 (0 = off, Z26)  */
   double reserved2[2]; /* must be zero                                                          */
 } ldu_solve_opts;
