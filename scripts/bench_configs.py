@@ -284,7 +284,7 @@ def c4(ldu, iters=300):
         dist.destroy_process_group()
 
 
-def c5dist(ldu, n=160, iters=200, slow_rank_sms=None):
+def c5dist(ldu, n=None, iters=200, slow_rank_sms=None):
     """NEXT-3 (Eq 5-8): the irregular mesh over N GPUs with (a) equal-cell
     slabs, (b) nnz-balanced slabs, (c) the paper's measured re-decomposition: per-rank speed
     s_i = (n_i + 2 o_i) / T_i from each rank's own kernel time T_i with the equal slabs (Eq 5),
@@ -298,6 +298,7 @@ def c5dist(ldu, n=160, iters=200, slow_rank_sms=None):
     uid = [ldu.Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = ldu.Comm(rank, world, uid[0], local)
+    n = n or int(os.environ.get("C5_N", "160"))
     g = meshgen.irregular_mesh(n, seed=1505)
     st = torch.cuda.current_stream()
     if slow_rank_sms and rank == 0:
