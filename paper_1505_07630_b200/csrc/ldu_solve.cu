@@ -1446,28 +1446,31 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
         p2p_pack_async(h, PACK_CG_P, h->r, s, GATE_LIVE);
         ++kernels;
       }
+      // the reduction protocol must be the same on every rank: with LL, every rank (also one
+      // without interfaces) finishes (p, q) in the fix-up kernel, which then has no cells
+      const bool fix = haveIf || h->cgLL;
       Red ra = red_loop(h, CTL_CG_A, false, h->gridA);
-      if (haveIf) ra.store_only = 1;
+      if (fix) ra.store_only = 1;
       prof_mark(h, profile, 4 * it + 0, s);
       launch_passA(h, ra, s);
       prof_mark(h, profile, 4 * it + 1, s);
       ++kernels;
-      if (haveIf) {
-        p2p_join(h, s);
+      if (fix) {
+        if (haveIf) p2p_join(h, s);
         Red ri = red_loop(h, CTL_CG_A, false);
-        const int ig = std::min(small_grid(h->nIfCells), h->maxParts - h->gridA);
+        const int ig = std::max(1, std::min(small_grid(h->nIfCells), h->maxParts - h->gridA));
         ri.slot_base = h->gridA;
         ri.total = h->gridA + ig;
         if (h->cgLL) {  // (p, q) as LL words; control A in the fix-up's last block
           ri.llctl = CTL_CG_A;
-          ri.llHalo = 1;
+          ri.llHalo = haveIf ? 1 : 0;
         }
         k_iface_cg_p2p<<<ig, kBlock, 0, s>>>(h->nIfCells, h->ifCell, h->ifCellPtr, h->ifFaceIdx,
                                              h->ifCoeffs, h->q, h->p0, h->p1, h->st, ri,
                                              h->p2pDesc, h->nIfFaces);
         ++kernels;
       }
-      if (!(h->cgLL && haveIf)) {
+      if (!h->cgLL) {
         k_ctl_p2p<<<1, 32, 0, s>>>(CTL_CG_A, h->st, h->p2pDesc, haveIf ? 1 : 0);
         ++kernels;
       }
