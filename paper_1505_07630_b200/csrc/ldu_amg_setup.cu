@@ -1612,7 +1612,13 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
     float ms = 0.f;
     CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
     H->setupMs = ms;
-    CUDA_CHECK(cudaMemPoolTrimTo(pool, 0));  // return the scratch to the device
+    // LDU_AMG_POOL_KEEP_MB > 0 keeps that much freed scratch mapped for the next setup: in a
+    // loop of setups 105 ms instead of 150-590 ms at 256^3, but inside bench.py one of two
+    // runs hit a 674 ms setup (profiles/r02_amg), so the default returns everything.  dmalloc
+    // trims the pool and retries if a later cudaMalloc finds the device full.
+    static const long long keepMB =
+        std::getenv("LDU_AMG_POOL_KEEP_MB") ? std::atoll(std::getenv("LDU_AMG_POOL_KEEP_MB")) : 0;
+    CUDA_CHECK(cudaMemPoolTrimTo(pool, (size_t)keepMB << 20));
   } catch (...) {
     cudaStreamSynchronize(s);
     cudaMemPoolTrimTo(pool, 0);

@@ -246,9 +246,19 @@ T* dmalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
   cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-  if (e != cudaSuccess) {
+  if (e != cudaSuccess) {  // the AMG setup keeps pool memory mapped: release it and retry once
     cudaGetLastError();
-    throw Error(LDU_ERR_OOM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(pool, 0);
+      e = cudaMalloc(&p, count * sizeof(T));
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(LDU_ERR_OOM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
+    }
   }
   return static_cast<T*>(p);
 }
