@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kBlock) k_iface_cg(int nIfCells, const int* __
 }
 
 enum Pack : int { PACK_PLAIN = 0, PACK_SCALED = 1, PACK_CG_P = 2, PACK_SCALED_W = 3, PACK_SCALED_LL = 4,
-                  PACK_SCALED_LL_W = 5 };
+                  PACK_SCALED_LL_W = 5, PACK_CG_P_LL = 6 };
 
 // Halo send buffer: the SpMV operand at the interface cells.
 __global__ void k_pack(int nIfFaces, const int* __restrict__ fc, int mode,
@@ -513,21 +513,21 @@ __global__ void __launch_bounds__(kBlock) k_pack_p2p(int nIfFaces, const int* __
   const int k = gateK ? *gateK : 0;
   double beta = 0.0;
   const double* pold = nullptr;
-  if (mode == PACK_CG_P) {  // classical: forked and joined between two control steps (no race)
+  if (mode == PACK_CG_P || mode == PACK_CG_P_LL) {  // classical: forked / joined between two control steps
     beta = st->beta;
     pold = (k & 1) ? p0 : p1;
   }
   const unsigned long long seq = d->seqHaloSend + 1;
   const int par = (int)(seq & 1);
   if (mode == PACK_SCALED_W || mode == PACK_SCALED_LL_W) a = (k & 1) ? p0 : p1;  // w_{i+1}
-  const bool ll = mode == PACK_SCALED_LL || mode == PACK_SCALED_LL_W;
+  const bool ll = mode == PACK_SCALED_LL || mode == PACK_SCALED_LL_W || mode == PACK_CG_P_LL;
   GRID_STRIDE(i, nIfFaces) {
     const int c = fc[i];
     double v = a[c];
-    if (mode == PACK_SCALED || mode == PACK_SCALED_W || ll) v = rD[c] * v;  // rD w
-    else if (mode == PACK_CG_P) v = fma(beta, pold[c], rD[c] * v);
+    if (mode == PACK_CG_P || mode == PACK_CG_P_LL) v = fma(beta, pold[c], rD[c] * v);
+    else if (mode != PACK_PLAIN) v = rD[c] * v;  // rD w
     const int kk = faceIf[i];
-    if (ll) {  // exchange 0 of the one-kernel loop: LL words, no flag (the flag release is skipped)
+    if (ll) {  // LL words (one-kernel loop, classical CG with cgLL): no flag release
       uint64_t* dst = mb_haloll(d->base[d->ifNeighbor[kk]], par, d->ifRemoteTotal[kk]);
       ll_store(dst + 2 * (size_t)(d->ifRemoteOff[kk] + (i - d->ifLocalOff[kk])), v, (uint32_t)seq);
     } else {
@@ -540,7 +540,8 @@ __global__ void __launch_bounds__(kBlock) k_pack_p2p(int nIfFaces, const int* __
   __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    if (ll) __threadfence();  // LL words carry their own sequence numbers: no system fence
+    else __threadfence_system();
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
@@ -582,9 +583,23 @@ __global__ void __launch_bounds__(kBlock) k_iface_cg_p2p(int nIfCells, const int
                                                          const double* p1, State* st, Red rd,
                                                          P2PDesc* d, int nIfFaces) {
   if (st->done) return;
-  const double* recv = p2p_wait_halo(d, nIfFaces);
   const double* __restrict__ pnew = (st->k & 1) ? p1 : p0;
   double v[1] = {0.0};
+  if (rd.llctl) {  // the halo came as LL words (PACK_CG_P_LL): each value carries its sequence number
+    const unsigned long long seq = d->seqHalo + 1;
+    const uint64_t* recv = mb_haloll(d->base[d->rank], (int)(seq & 1), nIfFaces);
+    GRID_STRIDE(i, nIfCells) {
+      double corr = 0.0;
+      for (int t = ptr[i]; t < ptr[i + 1]; ++t)
+        corr = fma(coeff[fidx[t]], ll_load(recv + 2 * (size_t)fidx[t], (uint32_t)seq), corr);
+      const int c = cell[i];
+      q[c] -= corr;
+      v[0] -= pnew[c] * corr;
+    }
+    finish_reduction_ll<1>(v, rd, st);
+    return;
+  }
+  const double* recv = p2p_wait_halo(d, nIfFaces);
   GRID_STRIDE(i, nIfCells) {
     double corr = 0.0;
     for (int t = ptr[i]; t < ptr[i + 1]; ++t) corr = fma(coeff[fidx[t]], __ldcv(recv + fidx[t]), corr);
@@ -592,8 +607,7 @@ __global__ void __launch_bounds__(kBlock) k_iface_cg_p2p(int nIfCells, const int
     q[c] -= corr;
     v[0] -= pnew[c] * corr;
   }
-  if (rd.llctl) finish_reduction_ll<1>(v, rd, st);
-  else finish_reduction<1>(v, rd, st);
+  finish_reduction<1>(v, rd, st);
 }
 
 // Multi-rank fused pipelined pass, fix-up of the interface rows once the halo has arrived:
@@ -1443,7 +1457,7 @@ long long enqueue_cg_iters(ldu_handle h, int batch, cudaStream_t s, bool profile
   if (mr && h->p2pOn) {  // halo and both reductions over NVLink peer memory, no NCCL kernels
     for (int it = 0; it < batch; ++it) {
       if (haveIf) {
-        p2p_pack_async(h, PACK_CG_P, h->r, s, GATE_LIVE);
+        p2p_pack_async(h, h->cgLL ? PACK_CG_P_LL : PACK_CG_P, h->r, s, GATE_LIVE);
         ++kernels;
       }
       // the reduction protocol must be the same on every rank: with LL, every rank (also one
