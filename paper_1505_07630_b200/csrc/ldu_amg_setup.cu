@@ -633,7 +633,9 @@ __global__ void k_lz_matvec(CsrView A, const double* __restrict__ sd, const doub
   block_store<1>(a, part);
 }
 
-// the same on the handle's own layout (level 0: DIA / SELL rows, coalesced, diagonal first)
+// the same on a coalesced layout: level 0 the handle's DIA / SELL rows (diagonal first, diag !=
+// NULL), coarse levels their SELL-32 copy (diagonal inside the rows, CSR order: the same sums as
+// k_lz_matvec)
 template <class Fmt>
 __global__ void k_lz_matvec_fmt(Fmt A, const double* __restrict__ diag, const double* __restrict__ sd,
                                 const double* __restrict__ v, const double* __restrict__ vprev,
@@ -641,7 +643,7 @@ __global__ void k_lz_matvec_fmt(Fmt A, const double* __restrict__ diag, const do
   const double b = *beta;
   double a[1] = {0.0};
   GSTRIDE(i, A.n) {
-    double acc = diag[i] * (sd[i] * v[i]);
+    double acc = diag ? diag[i] * (sd[i] * v[i]) : 0.0;
     for_row(A, (int)i, [&](int j, double aij) { acc += aij * (sd[j] * v[j]); });
     const double wi = sd[i] * acc - b * vprev[i];
     w[i] = wi;
@@ -736,6 +738,9 @@ double lanczos_omega(const CsrMat& A, const double* diag, int steps, cudaStream_
       with_layout(h0, [&](auto L) {
         k_lz_matvec_fmt<<<G, kSB, 0, s>>>(L, diag, sd, v, vp, scal + 1, w, part);
       });
+    else if (A.useSell)
+      k_lz_matvec_fmt<<<G, kSB, 0, s>>>(sell_view(A), (const double*)nullptr, sd, v, vp, scal + 1,
+                                         w, part);
     else
       k_lz_matvec<<<G, kSB, 0, s>>>(view(A), sd, v, vp, scal + 1, w, part);
     k_sum_parts<<<1, kSB, 0, s>>>(part, G, al + j);
