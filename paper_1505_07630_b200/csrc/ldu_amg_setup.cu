@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <type_traits>
 
 #include "ldu_amg.cuh"
@@ -45,19 +46,77 @@ int nblk(long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)(n); \
        i += (long long)gridDim.x * blockDim.x)
 
-// Stream-ordered scratch from the device's memory pool (cudaMallocAsync): the setup allocates
-// and frees tens of GB of temporaries level after level; plain cudaMalloc / cudaFree map and
-// unmap them every time (synchronous, and measured to vary 10x from run to run).  amg_setup
-// keeps the pool's memory until the hierarchy is built, then trims it.
+// Setup scratch.  The setup allocates and frees tens of GB of temporaries level after level, all
+// on one in-order stream.  Measured on B200 (profiles/r02_amg/malloc_probe.txt): growing the
+// stream-ordered pool (cudaMallocAsync beyond its reserve) costs 6-17 ms per GB with spikes to
+// 200 ms, and trimming it as much again, while a plain cudaMalloc of 3 GB takes ~1 ms.  So inside
+// amg_setup / dic_setup a ScratchCache hands out cudaMalloc'd blocks and takes them back when a
+// Scratch goes out of scope: a later request on the same stream reuses a free block (safe: every
+// earlier user of the block is ordered before it on s); the cache frees everything at the end.
+// Outside a cache (single-stage test entry points) Scratch uses the stream-ordered pool.
+struct ScratchCache {
+  std::multimap<size_t, void*> avail;  // free blocks by size
+  std::vector<void*> all;
+  void* get(size_t bytes) {
+    bytes = (bytes + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);  // 2 MB granules
+    auto it = avail.lower_bound(bytes);
+    if (it != avail.end() && it->first <= 2 * bytes + (8u << 20)) {
+      void* q = it->second;
+      avail.erase(it);
+      return q;
+    }
+    void* q = nullptr;
+    try {
+      q = dmalloc<char>(bytes);
+    } catch (const Error&) {  // device full: return the free blocks and retry once
+      cudaDeviceSynchronize();
+      for (auto& kv : avail) {
+        dfree(kv.second);
+        all.erase(std::find(all.begin(), all.end(), kv.second));
+        sizes.erase(kv.second);
+      }
+      avail.clear();
+      q = dmalloc<char>(bytes);
+    }
+    all.push_back(q);
+    sizes[q] = bytes;
+    return q;
+  }
+  void put(void* q) { avail.emplace(sizes[q], q); }
+  void release(cudaStream_t s) {
+    cudaStreamSynchronize(s);
+    for (void* q : all) dfree(q);
+    all.clear();
+    avail.clear();
+    sizes.clear();
+  }
+  std::map<void*, size_t> sizes;
+};
+thread_local ScratchCache* g_scratch = nullptr;
+
+struct ScratchScope {  // installs a cache for one setup; frees its blocks on exit
+  ScratchCache c;
+  ScratchCache* prev;
+  cudaStream_t s;
+  explicit ScratchScope(cudaStream_t st) : prev(g_scratch), s(st) { g_scratch = &c; }
+  ~ScratchScope() {
+    g_scratch = prev;
+    c.release(s);
+  }
+};
+
 struct Scratch {
   cudaStream_t s;
+  ScratchCache* cache;
   std::vector<void*> p;
-  explicit Scratch(cudaStream_t st) : s(st) {}
+  explicit Scratch(cudaStream_t st) : s(st), cache(g_scratch) {}
   template <class T>
   T* get(size_t n) {
     void* q = nullptr;
     const size_t bytes = std::max<size_t>(1, n) * sizeof(T);
-    if (cudaMallocAsync(&q, bytes, s) != cudaSuccess) {
+    if (cache) {
+      q = cache->get(bytes);
+    } else if (cudaMallocAsync(&q, bytes, s) != cudaSuccess) {
       cudaGetLastError();
       throw Error(LDU_ERR_OOM, "cudaMallocAsync of " + std::to_string(bytes) + " bytes failed");
     }
@@ -65,7 +124,10 @@ struct Scratch {
     return static_cast<T*>(q);
   }
   ~Scratch() {
-    for (void* q : p) cudaFreeAsync(q, s);
+    for (void* q : p) {
+      if (cache) cache->put(q);
+      else cudaFreeAsync(q, s);
+    }
   }
 };
 
@@ -1528,6 +1590,7 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
   H->opts = o;
   h->amg = H;
   try {
+    ScratchScope scratch(s);
     const int hashed = o.keyIndexOrder ? 0 : 1;
     PhaseTrace tr(s);
     g_trace = &tr;
@@ -1617,13 +1680,7 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
     float ms = 0.f;
     CUDA_CHECK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
     H->setupMs = ms;
-    // LDU_AMG_POOL_KEEP_MB > 0 keeps that much freed scratch mapped for the next setup: in a
-    // loop of setups 105 ms instead of 150-590 ms at 256^3, but inside bench.py one of two
-    // runs hit a 674 ms setup (profiles/r02_amg), so the default returns everything.  dmalloc
-    // trims the pool and retries if a later cudaMalloc finds the device full.
-    static const long long keepMB =
-        std::getenv("LDU_AMG_POOL_KEEP_MB") ? std::atoll(std::getenv("LDU_AMG_POOL_KEEP_MB")) : 0;
-    CUDA_CHECK(cudaMemPoolTrimTo(pool, (size_t)keepMB << 20));
+    CUDA_CHECK(cudaMemPoolTrimTo(pool, 0));  // scratch of the single-stage helpers, if any
   } catch (...) {
     cudaStreamSynchronize(s);
     cudaMemPoolTrimTo(pool, 0);
