@@ -676,10 +676,39 @@ __global__ void k_lz_scale(int n, double* __restrict__ v, const double* __restri
   GSTRIDE(i, n) v[i] = v[i] / nr;
 }
 
+// The Lanczos steps run without a host round trip: lz[0] = stopped (beta_j == 0), lz[1] = the
+// number of completed steps m; every kernel of a later step returns at once when stopped.
+__global__ void k_lz_sum_ctl(const double* __restrict__ part, int nparts, double* __restrict__ out,
+                             const int* lz) {
+  if (lz[0]) return;
+  __shared__ double sm[1][32];
+  double v[1];
+  sum_slots<1>(part, nparts, nparts, v);
+  block_reduce<1>(v, sm);
+  if (threadIdx.x == 0) out[0] = v[0];
+}
+// beta_j = sqrt((w, w)); the next step's beta; m = j + 1; stop on beta_j == 0
+__global__ void k_lz_beta(const double* __restrict__ part, int nparts, double* __restrict__ be_j,
+                          double* __restrict__ beta, int* lz, int j) {
+  if (lz[0]) return;
+  __shared__ double sm[1][32];
+  double v[1];
+  sum_slots<1>(part, nparts, nparts, v);
+  block_reduce<1>(v, sm);
+  if (threadIdx.x == 0) {
+    const double b = sqrt(v[0]);
+    *be_j = b;
+    *beta = b;
+    lz[1] = j + 1;
+    if (b == 0.0) lz[0] = 1;
+  }
+}
+
 // w = s .* (A (s .* v)) - beta v_prev; partial (w, v)
 __global__ void k_lz_matvec(CsrView A, const double* __restrict__ sd, const double* __restrict__ v,
                             const double* __restrict__ vprev, const double* __restrict__ beta,
-                            double* __restrict__ w, double* part) {
+                            double* __restrict__ w, double* part, const int* lz) {
+  if (lz[0]) return;
   const double b = *beta;
   double a[1] = {0.0};
   GSTRIDE(i, A.n) {
@@ -701,7 +730,9 @@ __global__ void k_lz_matvec(CsrView A, const double* __restrict__ sd, const doub
 template <class Fmt>
 __global__ void k_lz_matvec_fmt(Fmt A, const double* __restrict__ diag, const double* __restrict__ sd,
                                 const double* __restrict__ v, const double* __restrict__ vprev,
-                                const double* __restrict__ beta, double* __restrict__ w, double* part) {
+                                const double* __restrict__ beta, double* __restrict__ w, double* part,
+                                const int* lz) {
+  if (lz[0]) return;
   const double b = *beta;
   double a[1] = {0.0};
   GSTRIDE(i, A.n) {
@@ -716,7 +747,8 @@ __global__ void k_lz_matvec_fmt(Fmt A, const double* __restrict__ diag, const do
 
 // w -= alpha v; partial (w, w)
 __global__ void k_lz_orth(int n, double* __restrict__ w, const double* __restrict__ v,
-                          const double* __restrict__ alpha, double* part) {
+                          const double* __restrict__ alpha, double* part, const int* lz) {
+  if (lz[0]) return;
   const double al = *alpha;
   double a[1] = {0.0};
   GSTRIDE(i, n) {
@@ -729,7 +761,9 @@ __global__ void k_lz_orth(int n, double* __restrict__ w, const double* __restric
 
 // v_prev = v; v = w / beta
 __global__ void k_lz_next(int n, double* __restrict__ vprev, double* __restrict__ v,
-                          const double* __restrict__ w, const double* __restrict__ beta) {
+                          const double* __restrict__ w, const double* __restrict__ beta,
+                          const int* lz) {
+  if (lz[0]) return;
   const double b = *beta;
   GSTRIDE(i, n) {
     vprev[i] = v[i];
@@ -737,13 +771,13 @@ __global__ void k_lz_next(int n, double* __restrict__ vprev, double* __restrict_
   }
 }
 
-__global__ void k_sqrt(double* x) { x[0] = sqrt(x[0]); }
 
 // largest eigenvalue of the symmetric tridiagonal (alpha[0..m), beta[0..m-1)) by bisection on
 // the Sturm count; then w = (4/3) / (1.05 lambda) (reading Z27)
-__global__ void k_tridiag_max(int m, const double* __restrict__ al, const double* __restrict__ be,
-                              double* __restrict__ out) {
+__global__ void k_tridiag_max(const int* __restrict__ lz, const double* __restrict__ al,
+                              const double* __restrict__ be, double* __restrict__ out) {
   if (threadIdx.x || blockIdx.x) return;
+  const int m = lz[1];
   double lo = al[0], hi = al[0];
   for (int i = 0; i < m; ++i) {
     const double r = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < m ? fabs(be[i]) : 0.0);
@@ -794,29 +828,26 @@ double lanczos_omega(const CsrMat& A, const double* diag, int steps, cudaStream_
   k_lz_scale<<<G, kSB, 0, s>>>(n, v, scal);
   CUDA_CHECK(cudaMemsetAsync(vp, 0, sizeof(double) * n, s));
   CUDA_CHECK(cudaMemsetAsync(scal + 1, 0, sizeof(double), s));
-  int m = 0;
-  for (int j = 0; j < ms; ++j) {
+  int* lz = sc.get<int>(2);
+  CUDA_CHECK(cudaMemsetAsync(lz, 0, 2 * sizeof(int), s));
+  for (int j = 0; j < ms; ++j) {  // enqueued without a host round trip (stop flag on the device)
     if (h0)  // level 0: the handle's layout instead of the assembled CSR (same operator)
       with_layout(h0, [&](auto L) {
-        k_lz_matvec_fmt<<<G, kSB, 0, s>>>(L, diag, sd, v, vp, scal + 1, w, part);
+        k_lz_matvec_fmt<<<G, kSB, 0, s>>>(L, diag, sd, v, vp, scal + 1, w, part, lz);
       });
     else if (A.useSell)
       k_lz_matvec_fmt<<<G, kSB, 0, s>>>(sell_view(A), (const double*)nullptr, sd, v, vp, scal + 1,
-                                         w, part);
+                                         w, part, lz);
     else
-      k_lz_matvec<<<G, kSB, 0, s>>>(view(A), sd, v, vp, scal + 1, w, part);
-    k_sum_parts<<<1, kSB, 0, s>>>(part, G, al + j);
-    k_lz_orth<<<G, kSB, 0, s>>>(n, w, v, al + j, part);
-    k_sum_parts<<<1, kSB, 0, s>>>(part, G, be + j);
-    k_sqrt<<<1, 1, 0, s>>>(be + j);
+      k_lz_matvec<<<G, kSB, 0, s>>>(view(A), sd, v, vp, scal + 1, w, part, lz);
+    k_lz_sum_ctl<<<1, kSB, 0, s>>>(part, G, al + j, lz);
+    k_lz_orth<<<G, kSB, 0, s>>>(n, w, v, al + j, part, lz);
+    k_lz_beta<<<1, kSB, 0, s>>>(part, G, be + j, scal + 1, lz, j);
     CUDA_CHECK(cudaGetLastError());
-    m = j + 1;
-    const double bj = d2h(be + j, s);
-    if (bj == 0.0 || j == ms - 1) break;
-    CUDA_CHECK(cudaMemcpyAsync(scal + 1, be + j, sizeof(double), cudaMemcpyDeviceToDevice, s));
-    k_lz_next<<<G, kSB, 0, s>>>(n, vp, v, w, be + j);
+    if (j == ms - 1) break;
+    k_lz_next<<<G, kSB, 0, s>>>(n, vp, v, w, be + j, lz);
   }
-  k_tridiag_max<<<1, 1, 0, s>>>(m, al, be, scal + 2);
+  k_tridiag_max<<<1, 1, 0, s>>>(lz, al, be, scal + 2);
   CUDA_CHECK(cudaGetLastError());
   double res[2];
   CUDA_CHECK(cudaMemcpyAsync(res, scal + 2, sizeof(res), cudaMemcpyDeviceToHost, s));
