@@ -1259,10 +1259,14 @@ template <class B, int CAP, int G>
 bool spgemm_rows_cap(const CsrMat& A, B b, int ncols, bool drop, CsrMat& C, cudaStream_t s) {
   Scratch sc(s);
   const int n = A.nrows;
-  // measured at 256^3: narrow rows (A T, A P) are cheaper counted then written in place (a
-  // bound-spaced scratch scatters their few entries widely); wide rows (R (A P)) in one pass
+  // one pass into bound-spaced scratch, then packed.  Narrow rows (A T, A P) were cheaper counted
+  // then written in place while the scratch came from the stream-ordered pool (its growth cost
+  // dominated); with the cudaMalloc block cache one pass wins for them too (256^3 setup 109-114
+  // -> 100-103 ms).  LDU_AMG_GEMM_1PASS_NARROW=0 restores the two passes for narrow rows,
+  // LDU_AMG_GEMM_2PASS=1 for all.
   static const bool twoPass = std::getenv("LDU_AMG_GEMM_2PASS") && std::atoi(std::getenv("LDU_AMG_GEMM_2PASS")) != 0;
-  bool onePass = G == 32 && !twoPass;
+  static const bool narrow1 = !std::getenv("LDU_AMG_GEMM_1PASS_NARROW") || std::atoi(std::getenv("LDU_AMG_GEMM_1PASS_NARROW")) != 0;
+  bool onePass = (G == 32 || narrow1) && !twoPass;
   long long* toff = nullptr;
   int* toff32 = nullptr;
   int* tcol = nullptr;
