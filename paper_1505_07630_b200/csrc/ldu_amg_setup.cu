@@ -376,6 +376,26 @@ __device__ __forceinline__ void for_row(const SellView& A, int c, F f) {
   }
 }
 
+// The same visit order for a matrix-vector product: zero DIA coefficients are visited too (they
+// add an exact 0), so no load waits on a value test and the row's loads issue together.
+template <int ND, class F>
+__device__ __forceinline__ void for_row_mv(const DiaView<ND>& A, int c, F f) {
+#pragma unroll
+  for (int k = ND - 1; k >= 0; --k) {
+    const int j = c - A.off[k];
+    if (j >= 0) f(j, A.U[k][j]);
+  }
+#pragma unroll
+  for (int k = 0; k < ND; ++k) {
+    const int j = c + A.off[k];
+    if (j < A.n) f(j, A.U[k][c]);
+  }
+}
+template <class F>
+__device__ __forceinline__ void for_row_mv(const SellView& A, int c, F f) {
+  for_row(A, c, f);
+}
+
 template <class Fmt>
 __global__ void k_l0_count(Fmt A, long long* __restrict__ cnt) {
   GSTRIDE(c, A.n) {
@@ -737,7 +757,7 @@ __global__ void k_lz_matvec_fmt(Fmt A, const double* __restrict__ diag, const do
   double a[1] = {0.0};
   GSTRIDE(i, A.n) {
     double acc = diag ? diag[i] * (sd[i] * v[i]) : 0.0;
-    for_row(A, (int)i, [&](int j, double aij) { acc += aij * (sd[j] * v[j]); });
+    for_row_mv(A, (int)i, [&](int j, double aij) { acc += aij * (sd[j] * v[j]); });
     const double wi = sd[i] * acc - b * vprev[i];
     w[i] = wi;
     a[0] += wi * v[i];
