@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <type_traits>
 
 #include "ldu_amg.cuh"
@@ -46,61 +47,83 @@ int nblk(long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)(n); \
        i += (long long)gridDim.x * blockDim.x)
 
-// Setup scratch.  The setup allocates and frees tens of GB of temporaries level after level, all
+// Setup memory.  The setup allocates and frees tens of GB of temporaries level after level, all
 // on one in-order stream.  Measured on B200 (profiles/r02_amg/malloc_probe.txt): growing the
 // stream-ordered pool (cudaMallocAsync beyond its reserve) costs 6-17 ms per GB with spikes to
 // 200 ms, and trimming it as much again, while a plain cudaMalloc of 3 GB takes ~1 ms.  So inside
-// amg_setup / dic_setup a ScratchCache hands out cudaMalloc'd blocks and takes them back when a
-// Scratch goes out of scope: a later request on the same stream reuses a free block (safe: every
-// earlier user of the block is ordered before it on s); the cache frees everything at the end.
-// Outside a cache (single-stage test entry points) Scratch uses the stream-ordered pool.
-struct ScratchCache {
+// amg_setup a ScratchCache hands out cudaMalloc'd blocks and takes them back when a Scratch goes
+// out of scope: a later request on the same stream reuses a free block (safe: every earlier user
+// of the block is ordered before it on s).  It is also the AllocHook for the setup's dmalloc /
+// dfree: the previous hierarchy's buffers (amg_setup releases it under the hook) and the
+// intermediate products the setup frees become reusable blocks, and outputs may take one
+// (ownership passes to the hierarchy).  Whatever is left is freed at the end.  Outside a cache
+// (single-stage test entry points) Scratch uses the stream-ordered pool.
+struct ScratchCache : AllocHook {
   std::multimap<size_t, void*> avail;  // free blocks by size
-  std::vector<void*> all;
-  void* get(size_t bytes) {
-    bytes = (bytes + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);  // 2 MB granules
+  std::set<void*> owned;               // every block the cache owns (free or lent to a Scratch)
+  static size_t granule(size_t bytes) {
+    return (bytes + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);  // 2 MB granules
+  }
+  void* find(size_t bytes) {
     auto it = avail.lower_bound(bytes);
-    if (it != avail.end() && it->first <= 2 * bytes + (8u << 20)) {
-      void* q = it->second;
-      avail.erase(it);
-      return q;
-    }
-    void* q = nullptr;
-    try {
-      q = dmalloc<char>(bytes);
-    } catch (const Error&) {  // device full: return the free blocks and retry once
-      cudaDeviceSynchronize();
-      for (auto& kv : avail) {
-        dfree(kv.second);
-        all.erase(std::find(all.begin(), all.end(), kv.second));
-        sizes.erase(kv.second);
-      }
-      avail.clear();
-      q = dmalloc<char>(bytes);
-    }
-    all.push_back(q);
-    sizes[q] = bytes;
+    if (it == avail.end() || it->first > 2 * bytes + (8u << 20)) return nullptr;
+    void* q = it->second;
+    avail.erase(it);
     return q;
   }
-  void put(void* q) { avail.emplace(sizes[q], q); }
+  void* get(size_t bytes) {  // lent to a Scratch, returned by put
+    bytes = granule(bytes);
+    if (void* q = find(bytes)) return q;
+    void* q = nullptr;
+    try {
+      q = dmalloc_raw(bytes);
+    } catch (const Error&) {  // device full: free the idle blocks and retry once
+      trim();
+      q = dmalloc_raw(bytes);
+    }
+    owned.insert(q);
+    return q;
+  }
+  void put(void* q) { avail.emplace(alloc_size(q), q); }
+  void* take(size_t bytes) override {  // an output: ownership passes to the caller
+    void* q = find(bytes);
+    if (q) owned.erase(q);
+    return q;
+  }
+  bool give(void* p, size_t bytes) override {
+    owned.insert(p);
+    avail.emplace(bytes, p);
+    return true;
+  }
+  void trim() {
+    cudaDeviceSynchronize();
+    for (auto& kv : avail) {
+      owned.erase(kv.second);
+      dfree_raw(kv.second);
+    }
+    avail.clear();
+  }
   void release(cudaStream_t s) {
     cudaStreamSynchronize(s);
-    for (void* q : all) dfree(q);
-    all.clear();
+    for (void* q : owned) dfree_raw(q);
+    owned.clear();
     avail.clear();
-    sizes.clear();
   }
-  std::map<void*, size_t> sizes;
 };
 thread_local ScratchCache* g_scratch = nullptr;
 
-struct ScratchScope {  // installs a cache for one setup; frees its blocks on exit
+struct ScratchScope {  // installs a cache (and the dmalloc / dfree hook) for one setup
   ScratchCache c;
   ScratchCache* prev;
+  AllocHook* prevHook;
   cudaStream_t s;
-  explicit ScratchScope(cudaStream_t st) : prev(g_scratch), s(st) { g_scratch = &c; }
+  explicit ScratchScope(cudaStream_t st) : prev(g_scratch), prevHook(alloc_hook()), s(st) {
+    g_scratch = &c;
+    alloc_hook() = &c;
+  }
   ~ScratchScope() {
     g_scratch = prev;
+    alloc_hook() = prevHook;
     c.release(s);
   }
 };
@@ -1630,8 +1653,13 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
   if (!o.lanczosSteps) o.lanczosSteps = 20;
   if (!h->symmetric) fail_arg("AMG requires a symmetric matrix (lower == NULL or lower == upper)");
   // multi-rank: the hierarchy of the rank's local matrix (block-Jacobi, reading Z33)
-  amg_release(h);
   cudaStream_t s = h->own_stream;
+  // the previous hierarchy's buffers go to the setup's block cache (reused in stream order
+  // after one device synchronisation: solves on other streams may still read them)
+  ScratchScope scratch(s);
+  const bool had = h->amg != nullptr;
+  amg_release(h);
+  if (had) CUDA_CHECK(cudaDeviceSynchronize());
   cudaMemPool_t pool;
   CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, h->device));
   unsigned long long keep = ~0ULL;  // keep freed scratch mapped for reuse during the build
@@ -1645,7 +1673,6 @@ void amg_setup(ldu_handle h, const ldu_amg_opts* opts) {
   H->opts = o;
   h->amg = H;
   try {
-    ScratchScope scratch(s);
     const int hashed = o.keyIndexOrder ? 0 : 1;
     PhaseTrace tr(s);
     g_trace = &tr;

@@ -241,28 +241,38 @@ void configure(ldu_handle h);
 double stream_triad(int device, long long n, int reps);
 // memory helpers
 bool is_device_ptr(const void* p);
+// Device allocations go through dmalloc / dfree, which record each block's size.  While an
+// AllocHook is installed (the AMG setup's block cache, ldu_amg_setup.cu) dmalloc first asks it for
+// a cached block (ownership passes to the caller) and dfree hands freed blocks to it instead of
+// cudaFree -- a re-setup then reuses the previous hierarchy's memory in stream order.
+struct AllocHook {
+  virtual void* take(size_t bytes) = 0;          // a cached block of >= bytes, or nullptr
+  virtual bool give(void* p, size_t bytes) = 0;  // keep a freed block (true) or not
+  virtual ~AllocHook() {}
+};
+AllocHook*& alloc_hook();  // thread-local (ldu_setup.cu)
+void alloc_register(void* p, size_t bytes);
+size_t alloc_unregister(void* p);  // the block's size, 0 if unknown
+size_t alloc_size(void* p);
+void* dmalloc_raw(size_t bytes);  // cudaMalloc + register (trims the pool and retries once)
+inline void dfree_raw(void* p) {
+  if (!p) return;
+  alloc_unregister(p);
+  cudaFree(p);
+}
 template <class T>
 T* dmalloc(size_t count) {
-  void* p = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-  if (e != cudaSuccess) {  // the AMG setup keeps pool memory mapped: release it and retry once
-    cudaGetLastError();
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      cudaDeviceSynchronize();
-      cudaMemPoolTrimTo(pool, 0);
-      e = cudaMalloc(&p, count * sizeof(T));
-    }
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      throw Error(LDU_ERR_OOM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
-    }
-  }
-  return static_cast<T*>(p);
+  if (AllocHook* hk = alloc_hook())
+    if (void* q = hk->take(count * sizeof(T))) return static_cast<T*>(q);
+  return static_cast<T*>(dmalloc_raw(count * sizeof(T)));
 }
 inline void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (!p) return;
+  if (AllocHook* hk = alloc_hook()) {
+    const size_t b = alloc_size(p);
+    if (b && hk->give(p, b)) return;
+  }
+  dfree_raw(p);
 }
 }  // namespace ldu

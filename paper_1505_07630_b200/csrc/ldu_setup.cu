@@ -9,6 +9,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -17,6 +19,53 @@
 #include "ldu_impl.cuh"
 
 namespace ldu {
+
+namespace {
+std::mutex g_alloc_mu;
+std::unordered_map<void*, size_t> g_alloc_sizes;
+}  // namespace
+AllocHook*& alloc_hook() {
+  static thread_local AllocHook* hk = nullptr;
+  return hk;
+}
+void alloc_register(void* p, size_t bytes) {
+  std::lock_guard<std::mutex> g(g_alloc_mu);
+  g_alloc_sizes[p] = bytes;
+}
+size_t alloc_unregister(void* p) {
+  std::lock_guard<std::mutex> g(g_alloc_mu);
+  auto it = g_alloc_sizes.find(p);
+  if (it == g_alloc_sizes.end()) return 0;
+  const size_t b = it->second;
+  g_alloc_sizes.erase(it);
+  return b;
+}
+size_t alloc_size(void* p) {
+  std::lock_guard<std::mutex> g(g_alloc_mu);
+  auto it = g_alloc_sizes.find(p);
+  return it == g_alloc_sizes.end() ? 0 : it->second;
+}
+void* dmalloc_raw(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 1;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {  // stream-ordered pool memory may still be mapped: release it, retry once
+    cudaGetLastError();
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(pool, 0);
+      e = cudaMalloc(&p, bytes);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(LDU_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    }
+  }
+  alloc_register(p, bytes);
+  return p;
+}
 
 bool is_device_ptr(const void* p) {
   if (!p) return false;
