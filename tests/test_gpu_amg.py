@@ -353,3 +353,58 @@ def test_setup_paths_are_bitwise_identical(ldu, tmp_path):
         assert sorted(res["0"].files) == sorted(res[other].files)
         for k in res["0"].files:
             np.testing.assert_array_equal(res["0"][k], res[other][k], err_msg=f"{other} {k}")
+
+
+def _dump_hierarchy(A):
+    info = A.amg_info()
+    out = {"n": list(info["n"])}
+    for l in range(info["nLevels"] + 1):
+        for w in ("A",) + (("P", "R") if l < info["nLevels"] else ()):
+            out[f"{w}{l}"] = tuple(np.array(a, copy=True) for a in A.amg_matrix(l, w))
+    for l in range(info["nLevels"]):
+        out[f"agg{l}"] = np.array(A.amg_aggregates(l), copy=True)
+    return out
+
+
+def _assert_same_hierarchy(h, f, what):
+    assert h["n"] == f["n"], what
+    assert sorted(h) == sorted(f), what
+    for k in h:
+        if k == "n":
+            continue
+        a, b = h[k], f[k]
+        if isinstance(a, tuple):
+            for x, y in zip(a, b):
+                np.testing.assert_array_equal(x, y, err_msg=f"{what} {k}")
+        else:
+            np.testing.assert_array_equal(a, b, err_msg=f"{what} {k}")
+
+
+def test_resetup_reuses_memory_bitwise(ldu):
+    """A re-setup on the same handle builds its hierarchy in the previous hierarchy's memory (the
+    setup's block cache is the dmalloc / dfree hook).  Alternating option sets leave different
+    contents in the reused blocks, so any read of stale data shows up: every re-setup must equal a
+    fresh handle's build bit for bit, and so must the solve on it."""
+    s = meshgen.hex_laplacian(40, 36, 30, conductance_sigma=0.5, seed=11)
+    variants = [dict(), dict(unsmoothed=True), dict(keyIndexOrder=True), dict()]
+    fresh = {}
+    for v in variants:
+        key = tuple(sorted(v.items()))
+        if key in fresh:
+            continue
+        with ldu.LduMatrix.from_system(s) as F:
+            F.amg_setup(**v)
+            fresh[key] = _dump_hierarchy(F)
+    b = cuda(np.random.default_rng(5).uniform(-1, 1, s.nCells))
+    with ldu.LduMatrix.from_system(s) as A, ldu.LduMatrix.from_system(s) as F:
+        for i, v in enumerate(variants):
+            A.amg_setup(**v)
+            _assert_same_hierarchy(_dump_hierarchy(A), fresh[tuple(sorted(v.items()))],
+                                   f"re-setup {i} {v}")
+        F.amg_setup()
+        xa = torch.zeros(s.nCells, dtype=torch.float64, device="cuda")
+        xf = torch.zeros_like(xa)
+        ra = A.amg_pcg_solve(b, xa, tol=1e-10, maxIter=200)
+        rf = F.amg_pcg_solve(b, xf, tol=1e-10, maxIter=200)
+        assert ra == rf
+        assert torch.equal(xa, xf)
