@@ -51,7 +51,9 @@ def parse():
     p.add_argument("--amg-tol", type=float, default=1e-8)
     p.add_argument("--no-c5", action="store_true",
                    help="skip the c5 irregular (SELL-32) evidence leg")
-    p.add_argument("--c5-n", type=int, default=160, help="c5 leg: irregular mesh base n^3")
+    p.add_argument("--c5-n", type=int, default=184,
+                   help="c5 leg: irregular mesh base n^3 (184^3 = 6.2M cells: one GPU's share of "
+                        "config 5's 50M cells on 8 GPUs)")
     return p.parse_args()
 
 
@@ -556,7 +558,7 @@ def main():
                           "frac": vb / (vc_ms / 1e3) / 1e9 / peak, "bound": "hbm",
                           "peak_source": peak_src}}
 
-    # c5 evidence leg (SURVEY §8(d) config 5 recipe at a reduced base size, 1 GPU): the irregular
+    # c5 evidence leg (SURVEY §8(d) config 5 recipe at one GPU's share of its 50M cells): the irregular
     # RCM mesh on the SELL-32 layout, fixed iterations, live per-launch time of the fused pass
     # against the bytes the SELL-32 layout must move (12 B per stored entry incl. padding)
     c5 = None
@@ -568,7 +570,8 @@ def main():
         b5 = torch.from_numpy(g5.b).cuda()
         x5 = torch.zeros_like(b5)
         c5 = {"workload": f"c5 recipe, irregular {args.c5_n}^3 base ({g5.nCells:,} cells, "
-                          f"{g5.nFaces:,} faces), RCM order", "layout": i5["layout_name"],
+                          f"{g5.nFaces:,} faces), RCM order; config 5 is 50M cells on 8 GPUs, "
+                          f"i.e. 6.25M per GPU", "layout": i5["layout_name"],
               "stored_entries_per_row": i5["storedEntries"] / g5.nCells}
         for solver in ("pipecg", "pcg"):
             fn5 = A5.pcg_solve if solver == "pcg" else A5.pipecg_solve
