@@ -5,7 +5,8 @@ batches exit early on the device `done` flag, against the oracle on the same see
 Bars (BASELINE.json north_star): solution rel-L2 <= 1e-8 at tol 1e-10; iteration counts within
 +-2 %.  Configs: c3-like 96^3 / 128^3 Poisson (DIA layout) with both criteria (reading Z1) and
 x0 = 0 / x0 != 0; c5-like irregular RCM mesh at 80^3 base (SELL-32 layout, > 2 wavefronts); the
-c2 icoFoam pressure sequence (warm-started, OpenFOAM norm) on the 512^2 cavity."""
+c2 icoFoam pressure sequence (warm-started, OpenFOAM norm) on the 512^2 cavity; c2 at its full
+1024^2 size solved to its tolerance (PCG) and 60 fixed iterations of both solvers."""
 import numpy as np
 import pytest
 
