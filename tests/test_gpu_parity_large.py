@@ -171,3 +171,32 @@ def test_cavity_1024_to_tolerance():
     assert st == ldu.OK and res < 1e-6 and ores < 1e-6
     assert abs(it - oit) <= max(1, round(0.02 * oit)), (it, oit)
     assert rel(x.cpu().numpy(), ox) <= 1e-5
+
+
+@pytest.mark.parametrize("solver", ["pcg", "pipecg"])
+def test_c5_share_184_sampled(ldu, solver):
+    """Config 5's recipe at one GPU's share of its 50M cells (184^3 base, 6.2M cells, RCM,
+    SELL-32), the mesh and launch configuration of bench.py's c5 leg: SpMV over all rows vs the
+    oracle; 30 fixed iterations vs the oracle's 30; then a solve to 1e-10 whose true residual
+    (recomputed by the oracle's SpMV) meets the tolerance within the pipelined recurrence gap."""
+    s = meshgen.irregular_mesh(184, seed=1505)
+    xr = np.random.default_rng(5).uniform(-1, 1, s.nCells)
+    ofn = oracle.pcg if solver == "pcg" else oracle.pipecg
+    ost, ox, oit, ores = ofn(s, s.b, tol=0.0, maxIter=30)
+    with ldu.LduMatrix.from_system(s) as A:
+        assert A.info()["layout_name"] == "SELL32"
+        y = torch.empty(s.nCells, dtype=torch.float64, device="cuda")
+        A.amul(cuda(xr), y)
+        assert rel(y.cpu().numpy(), oracle.amul(s, xr)) <= 1e-12
+        fn = A.pcg_solve if solver == "pcg" else A.pipecg_solve
+        x = torch.zeros(s.nCells, dtype=torch.float64, device="cuda")
+        st, it, res = fn(cuda(s.b), x, tol=0.0, maxIter=30)
+        assert it == oit == 30
+        assert rel(x.cpu().numpy(), ox) <= 1e-10
+        assert abs(res - ores) <= 1e-8 * ores
+        x.zero_()
+        st, it, res = fn(cuda(s.b), x, tol=1e-10, maxIter=100000)
+    assert st == ldu.OK and res < 1e-10
+    xg = x.cpu().numpy()
+    true = np.linalg.norm(s.b - oracle.amul(s, xg)) / np.linalg.norm(s.b)
+    assert true < 1e-9, true
