@@ -6,7 +6,8 @@ Bars (BASELINE.json north_star): solution rel-L2 <= 1e-8 at tol 1e-10; iteration
 +-2 %.  Configs: c3-like 96^3 / 128^3 Poisson (DIA layout) with both criteria (reading Z1) and
 x0 = 0 / x0 != 0; c5-like irregular RCM mesh at 80^3 base (SELL-32 layout, > 2 wavefronts); the
 c2 icoFoam pressure sequence (warm-started, OpenFOAM norm) on the 512^2 cavity; c2 at its full
-1024^2 size solved to its tolerance (PCG) and 60 fixed iterations of both solvers."""
+1024^2 size solved to its tolerance (PCG) and 60 fixed iterations of both solvers; config 5 at one
+GPU's share (184^3 irregular, SELL-32) and config 4 at full size on one GPU (512^3) sampled."""
 import numpy as np
 import pytest
 
@@ -200,3 +201,25 @@ def test_c5_share_184_sampled(ldu, solver):
     xg = x.cpu().numpy()
     true = np.linalg.norm(s.b - oracle.amul(s, xg)) / np.linalg.norm(s.b)
     assert true < 1e-9, true
+
+
+def test_c4_512_cube_sampled(ldu):
+    """Config 4 at its full size on one GPU (512^3, 134M cells: the N = 1 point of the 1/2/4/8
+    scaling run): SpMV over all rows vs the oracle, and 5 fixed pipelined iterations vs the
+    oracle's 5 (the oracle needs ~1 min for them at this size)."""
+    n = 512
+    s = meshgen.hex_laplacian(n, n, n)
+    b = meshgen.rhs_hot_face(n, n, n)
+    xr = np.random.default_rng(3).uniform(-1, 1, s.nCells)
+    yo = oracle.amul(s, xr)
+    ost, ox, oit, ores = oracle.pipecg(s, b, tol=0.0, maxIter=5)
+    with ldu.LduMatrix.from_system(s) as A:
+        y = torch.empty(s.nCells, dtype=torch.float64, device="cuda")
+        A.amul(cuda(xr), y)
+        assert rel(y.cpu().numpy(), yo) <= 1e-12
+        del y
+        x = torch.zeros(s.nCells, dtype=torch.float64, device="cuda")
+        st, it, res = A.pipecg_solve(cuda(b), x, tol=0.0, maxIter=5)
+    assert it == oit == 5
+    assert rel(x.cpu().numpy(), ox) <= 1e-10
+    assert abs(res - ores) <= 1e-8 * ores
