@@ -91,7 +91,7 @@ struct ScratchCache : AllocHook {
     return q;
   }
   bool give(void* p, size_t bytes) override {
-    owned.insert(p);
+    if (!owned.insert(p).second) return true;  // already cached (a repeated free): keep one entry
     avail.emplace(bytes, p);
     return true;
   }
